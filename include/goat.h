@@ -1,0 +1,159 @@
+/*
+ * goat.h -- C ABI of libgoat.so, the B200 (sm_100a) GOAT iteration.
+ *
+ * GOAT (arXiv 2111.05366) is Frank-Wolfe graph matching whose per-iteration
+ * linear-assignment step is replaced by entropic Sinkhorn OT ("LOT").  The
+ * reference (`otmatch`, pure Python/numpy) has no plugin registry; its one
+ * strategy seam is the Frank-Wolfe core
+ *     _fw_core(A, B, L, P0, opts) -> (assignment, history, iterations, converged)
+ *     /root/reference/pkg/src/otmatch/matcher.py:177-212
+ * which is what goat_fw_core() replaces.  The component entry points below
+ * replace the functions _fw_core calls, so the reference's own component tests
+ * can be restated against them.  Everything here takes plain pointers and
+ * sizes; host matrices are float64 row-major with a leading dimension, exactly
+ * the numpy arrays the reference passes (core.py:22).  The library never keeps
+ * caller pointers after a call returns and never mutates inputs.
+ *
+ * Errors: every function returns GOAT_OK (0) or a GOAT_E* code; the message is
+ * available from goat_last_error() (thread-local).  GOAT_EINVAL corresponds to
+ * the reference's ValueError (core.py:23-26, matcher.py:52-66,105-106).
+ * Sinkhorn non-convergence is NOT an error (sinkhorn.py:85).
+ *
+ * Threading: a handle is bound to one device and one stream and must not be
+ * used from two threads at once; distinct handles may run concurrently.
+ */
+#ifndef GOAT_H
+#define GOAT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GOAT_OK 0
+#define GOAT_EINVAL 1  /* invalid argument (reference: ValueError) */
+#define GOAT_ECUDA 2   /* CUDA runtime / launch failure */
+#define GOAT_EOOM 3    /* device allocation failed */
+#define GOAT_ENOTSUP 4 /* unsupported configuration */
+
+#define GOAT_FP32 0    /* fp32 iterate, fp64 potentials and accumulators */
+#define GOAT_FP64 1    /* fp64 throughout (reference arithmetic) */
+
+#define GOAT_MINIMIZE 0
+#define GOAT_MAXIMIZE 1
+
+#define GOAT_STEP_EXACT_LAP 0 /* FAQ: matcher.py:191-192 */
+#define GOAT_STEP_LOT 1       /* GOAT: matcher.py:193-194 */
+
+/* GEMM engines for the gradient products (fp32 mode only; fp64 always SIMT). */
+#define GOAT_GEMM_AUTO 0
+#define GOAT_GEMM_SIMT 1     /* CUDA-core fp32 FMA */
+#define GOAT_GEMM_TCGEN05 2  /* tcgen05/TMEM/TMA bf16-split, fp32 accumulate */
+
+typedef struct goat_handle goat_handle;
+
+typedef struct goat_config {
+    int32_t device;     /* CUDA ordinal */
+    int32_t precision;  /* GOAT_FP32 | GOAT_FP64 */
+    int32_t gemm;       /* GOAT_GEMM_* */
+    int32_t split_terms;/* bf16 terms per non-exact operand for GOAT_GEMM_TCGEN05 (2 or 3; 0 = default 3) */
+} goat_config;
+
+/* MatchOptions (matcher.py:32-50) + SinkhornParams (sinkhorn.py:21-32). */
+typedef struct goat_options {
+    int32_t max_iters;    /* matcher.py:45 (30) */
+    int32_t max_sweeps;   /* sinkhorn.py:31 (1000) */
+    int32_t sense;        /* GOAT_MAXIMIZE (matcher.py:50) */
+    int32_t step_solver;  /* GOAT_STEP_LOT for GOAT */
+    double fw_tol;        /* matcher.py:46 (1e-2) */
+    double lam;           /* sinkhorn.py:30 (100) -- reg = 1/lam on the unit-range cost */
+    double sk_tol;        /* sinkhorn.py:32 (1e-8) */
+} goat_options;
+
+/* _fw_core's return value plus the diagnostics the reference discards. */
+typedef struct goat_fw_result {
+    int64_t *assignment;     /* [n] out: permutation p[row] = col (lap.py:56-57) */
+    double *hist_obj;        /* [max_iters+1] out: f(P_i), history[i][1] */
+    double *hist_alpha;      /* [max_iters+1] out: alpha_i (entry 0 = NaN) */
+    int32_t *lot_sweeps;     /* [max_iters] out or NULL */
+    int32_t *lot_converged;  /* [max_iters] out or NULL */
+    double *lot_dev;         /* [max_iters] out or NULL */
+    int32_t iterations;      /* out */
+    int32_t converged;       /* out */
+    int32_t lap_certified;   /* out: 1 if the O(n^2) strict-argmax certificate fired */
+    int32_t gpu_launches;    /* out: kernels launched by this call */
+    double objective;        /* out: sum_ij A_ij B_{p(i)p(j)} on the inputs (core.py:120-124) */
+    double time_ms[6];       /* out: gradient, lot, linesearch+update, lap, h2d+setup, total */
+} goat_fw_result;
+
+int goat_create(goat_handle **out, const goat_config *cfg);
+int goat_destroy(goat_handle *h);
+const char *goat_last_error(void);
+/* Reserve device workspace for order n up front (optional). */
+int goat_reserve(goat_handle *h, int64_t n);
+
+/* matcher.py:177-212 _fw_core on host float64 buffers.
+ * L: seeded linear term (matcher.py:267) or NULL.  P0: initial iterate or NULL
+ * for the barycenter J/n (core.py:89-93). */
+int goat_fw_core(goat_handle *h, int64_t n,
+                 const double *A, int64_t lda, const double *B, int64_t ldb,
+                 const double *L, int64_t ldl, const double *P0, int64_t ldp,
+                 const goat_options *opts, goat_fw_result *res);
+
+/* Same, inputs already resident on the handle's device (row-major, element
+ * type = the handle's precision: float for GOAT_FP32, double for GOAT_FP64). */
+int goat_fw_core_device(goat_handle *h, int64_t n,
+                        const void *dA, int64_t lda, const void *dB, int64_t ldb,
+                        const void *dL, int64_t ldl, const void *dP0, int64_t ldp,
+                        const goat_options *opts, goat_fw_result *res);
+
+/* matcher.py:100-107  G = A P B^T + A^T P B  (host float64 in/out). */
+int goat_gradient(goat_handle *h, int64_t n, const double *A, int64_t lda,
+                  const double *B, int64_t ldb, const double *P, int64_t ldp,
+                  double *G, int64_t ldg);
+
+/* sinkhorn.py:103-130  lot(M, sense, params) -> Q, converged, sweeps, deviation. */
+int goat_lot(goat_handle *h, int64_t n, const double *M, int64_t ldm, int32_t sense,
+             double lam, int32_t max_sweeps, double tol, double *Q, int64_t ldq,
+             int32_t *converged, int32_t *sweeps, double *deviation);
+
+/* sinkhorn.py:60-85  sinkhorn_knopp(K, params) on a strictly positive K. */
+int goat_sinkhorn_knopp(goat_handle *h, int64_t n, const double *K, int64_t ldk,
+                        int32_t max_sweeps, double tol, double *Q, int64_t ldq,
+                        int32_t *converged, int32_t *sweeps, double *deviation);
+
+/* matcher.py:110-122  (c2, c1) of the exact line search; L may be NULL. */
+int goat_line_search_coeffs(goat_handle *h, int64_t n, const double *A, int64_t lda,
+                            const double *B, int64_t ldb, const double *L, int64_t ldl,
+                            const double *P, int64_t ldp, const double *Q, int64_t ldq,
+                            double *c2, double *c1);
+
+/* lap.py:48-58  solve_lap(M, sense): exact LAP on device (certificate fast
+ * path, else the shortest-augmenting-path solver with scipy's visiting order). */
+int goat_lap(goat_handle *h, int64_t n, const double *M, int64_t ldm, int32_t sense,
+             int64_t *assignment, double *objective, int32_t *certified);
+
+/* core.py:120-124  sum_ij A_ij B_{p(i) p(j)} (fp64, fixed reduction order). */
+int goat_qap_objective_perm(goat_handle *h, int64_t n, const double *A, int64_t lda,
+                            const double *B, int64_t ldb, const int64_t *perm,
+                            double *objective);
+
+/* Run subsequent work of this handle on `stream` (a cudaStream_t; NULL = the
+ * handle's own stream).  Lets a caller bracket calls with its own CUDA events. */
+int goat_set_stream(goat_handle *h, void *stream);
+
+/* Measurement hook (bench.py roofline): `reps` back-to-back launches of the
+ * fused Sinkhorn sweep kernel over the device matrix G (handle precision,
+ * leading dim ld) at a mid-run sweep index; *ms_per_sweep = mean kernel time
+ * from CUDA events on the handle's stream.  Algorithmic bytes per launch = n*n*elem. */
+int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int32_t reps,
+                     double *ms_per_sweep);
+
+/* Library build/feature string, e.g. "goat sm_100a tcgen05". */
+const char *goat_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GOAT_H */

@@ -1,0 +1,796 @@
+// libgoat C ABI: handle management and the Frank-Wolfe (GOAT) orchestration.
+//
+// goat_fw_core replaces _fw_core (matcher.py:177-212).  Per outer iteration the
+// reference does 10 n^3 dgemm-class products (gradient 4, line search 4,
+// objective 2).  Here the gradient is carried by linearity
+//     G(P_{k+1}) = a G(P_k) + (1-a) G(Q_k)                     (matcher.py:197)
+// so only G(Q_k) = A Q B^T + A^T Q B is new (2 products when A, B are
+// symmetric, 4 otherwise), and the line-search coefficients and the logged
+// objective come from dot products against it:
+//     t1 = <G(Q), P> = s_PQ + s_QP,   s_QQ = <G(Q), Q> / 2,   s_PP = f(P)
+//     c2 = s_PP - t1 + s_QQ,          c1 = t1 - 2 s_QQ (+ <L, P - Q>)
+//     f(aP + (1-a)Q) = a^2 s_PP + a(1-a) t1 + (1-a)^2 s_QQ (+ a<L,P> + (1-a)<L,Q>)
+// (identities of matcher.py:110-122 and :170-174, all accumulated in fp64).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace goat {
+
+long &launch_count() {
+    static thread_local long c = 0;
+    return c;
+}
+
+static thread_local std::string g_last_error;
+
+struct Handle {
+    int device = 0;
+    int precision = GOAT_FP64;
+    int gemm = GOAT_GEMM_AUTO;
+    int split = 3;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    // workspace (sized for the largest order seen)
+    int64_t cap_n = 0;
+    DevBuf A, B, P, Q, G, GQ, T1, L, Gl, M;     // element = precision
+    DevBuf A64, B64, stage;                     // fp64 inputs (objective) + upload staging
+    DevBuf f[2], g[2], colpart, devpart, devcol, state, red, scal, vec, ivec;
+    DevBuf lap_d[3], lap_i[4], lap_b[2], lap_misc;
+    double *h_scal = nullptr;                   // pinned host scalars
+    SkState *h_state = nullptr;                 // pinned
+    ~Handle() {
+        if (h_scal) cudaFreeHost(h_scal);
+        if (h_state) cudaFreeHost(h_state);
+        if (own_stream) cudaStreamDestroy(own_stream);
+    }
+};
+
+namespace {
+
+
+inline int64_t ld_for(int64_t n) { return round_up(std::max<int64_t>(n, 1), 8); }
+
+void ensure_workspace(Handle &h, int64_t n) {
+    GOAT_CUDA(cudaSetDevice(h.device));
+    if (n <= h.cap_n) return;
+    const int64_t ld = ld_for(n);
+    const size_t es = h.precision == GOAT_FP32 ? 4 : 8;
+    const size_t mat = (size_t)n * ld * es;
+    for (DevBuf *b : {&h.A, &h.B, &h.P, &h.Q, &h.G, &h.GQ, &h.T1, &h.M}) b->ensure(mat);
+    const size_t vec = (size_t)ld * 8;
+    for (int s = 0; s < 2; ++s) { h.f[s].ensure(vec); h.g[s].ensure(vec); }
+    h.vec.ensure(vec * 4);
+    h.ivec.ensure((size_t)ld * 4 * 4);
+    h.devpart.ensure(4096 * 8);
+    h.devcol.ensure((size_t)(ld / kThreads + 2) * 8);
+    h.state.ensure(sizeof(SkState));
+    h.red.ensure(kRedBlocks * 8 * 8);
+    h.scal.ensure(64 * 8);
+    const size_t cp = h.precision == GOAT_FP32 ? sk_plan<float>((int)n, h.num_sms).colpart_bytes
+                                               : sk_plan<double>((int)n, h.num_sms).colpart_bytes;
+    h.colpart.ensure(cp);
+    for (int s = 0; s < 3; ++s) h.lap_d[s].ensure(vec);
+    for (int s = 0; s < 4; ++s) h.lap_i[s].ensure((size_t)ld * 4);
+    for (int s = 0; s < 2; ++s) h.lap_b[s].ensure((size_t)ld);
+    h.lap_misc.ensure(64);
+    h.cap_n = n;
+}
+
+void ensure_f64_inputs(Handle &h, int64_t n) {
+    const size_t mat = (size_t)n * ld_for(n) * 8;
+    h.A64.ensure(mat);
+    h.B64.ensure(mat);
+    h.stage.ensure(mat);
+}
+
+struct Ctx {
+    Handle &h;
+    int n;
+    int64_t ld;
+    cudaStream_t s;
+    bool sym = false;
+    Ctx(Handle &hh, int nn) : h(hh), n(nn), ld(ld_for(nn)), s(hh.stream) {}
+};
+
+// Upload a host fp64 matrix (leading dim lds) into dst (precision T, ld).
+template <class T>
+void upload(Ctx &c, const double *src, int64_t lds, T *dst, double *stage64) {
+    GOAT_CUDA(cudaMemcpy2DAsync(stage64, c.ld * 8, src, lds * 8, (size_t)c.n * 8, c.n,
+                                cudaMemcpyHostToDevice, c.s));
+    launch_convert<T>(stage64, c.ld, dst, c.ld, c.n, 1.0, c.s);  // also zeroes the padding
+}
+
+template <class T> void download(Ctx &c, const T *src, double *dst, int64_t ldd, double *stage64) {
+    launch_convert_to_f64<T>(src, c.ld, stage64, c.ld, c.n, c.s);
+    GOAT_CUDA(cudaMemcpy2DAsync(dst, ldd * 8, stage64, c.ld * 8, (size_t)c.n * 8, c.n,
+                                cudaMemcpyDeviceToHost, c.s));
+    GOAT_CUDA(cudaStreamSynchronize(c.s));
+}
+
+void sync(Ctx &c) { GOAT_CUDA(cudaStreamSynchronize(c.s)); }
+
+// ------------------------------------------------------------------ gradient
+// out = A X B^T + A^T X B (matcher.py:107); symmetric inputs: 2 A X B.
+template <class T>
+void gradient(Ctx &c, const T *A, const T *B, const T *X, T *out, T *tmp) {
+    const int n = c.n;
+    const int64_t ld = c.ld;
+    if (c.sym) {
+        gemm_simt<T>(n, n, n, 1.0, X, ld, 0, B, ld, 0, 0.0, tmp, ld, c.s);
+        gemm_simt<T>(n, n, n, 2.0, A, ld, 0, tmp, ld, 0, 0.0, out, ld, c.s);
+    } else {
+        gemm_simt<T>(n, n, n, 1.0, X, ld, 0, B, ld, 1, 0.0, tmp, ld, c.s);  // X B^T
+        gemm_simt<T>(n, n, n, 1.0, A, ld, 0, tmp, ld, 0, 0.0, out, ld, c.s);  // A (X B^T)
+        gemm_simt<T>(n, n, n, 1.0, X, ld, 0, B, ld, 0, 0.0, tmp, ld, c.s);  // X B
+        gemm_simt<T>(n, n, n, 1.0, A, ld, 1, tmp, ld, 0, 1.0, out, ld, c.s);  // + A^T (X B)
+    }
+}
+
+template <class T> bool is_symmetric(Ctx &c, const T *X) {
+    int *flag = c.h.ivec.as<int>();
+    const int one = 1;
+    GOAT_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, c.s));
+    launch_is_symmetric<T>(X, c.ld, c.n, flag, c.s);
+    int r = 0;
+    GOAT_CUDA(cudaMemcpyAsync(&r, flag, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    return r != 0;
+}
+
+// ------------------------------------------------------------------ LOT
+struct LotOut {
+    int sweeps = 0, converged = 0;
+    double dev = 0.0;
+    double nrm = 0.0;  // sum (Q - P)^2 (when P given)
+    double lq = 0.0;   // <L, Q> (when L given)
+    bool used_kernel = true;
+};
+
+// mode: 0 = lot(M) (sinkhorn.py:103-130); 1 = sinkhorn_knopp on K = exp(-Gin)
+template <class T>
+LotOut run_lot(Ctx &c, const T *Gin, int sense, double lam, int max_sweeps, double tol, T *Q,
+               const T *P, const T *L, int mode) {
+    Handle &h = c.h;
+    const int n = c.n;
+    LotOut out;
+    double gmax = 0.0, coef = 1.0;
+    int log_mode = 0;
+    if (mode == 0) {
+        double *mm = h.scal.as<double>();
+        launch_minmax<T>(Gin, c.ld, n, h.red.as<double>(), mm, c.s);
+        GOAT_CUDA(cudaMemcpyAsync(h.h_scal, mm, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        sync(c);
+        const double lo = h.h_scal[0], hi = h.h_scal[1];
+        const double scale = hi - lo;  // == shifted.max() (sinkhorn.py:115-119)
+        if (scale == 0.0) {            // sinkhorn.py:121-124: exact barycenter, 0 sweeps
+            launch_fill<T>(Q, c.ld, n, 1.0 / n, c.s);
+            out.sweeps = 0; out.converged = 1; out.dev = 0.0;
+            out.used_kernel = false;
+            return out;
+        }
+        const bool maximize = (sense == GOAT_MAXIMIZE);
+        gmax = maximize ? hi : lo;
+        coef = maximize ? -lam / scale : lam / scale;
+        // sinkhorn.py:127: K.min() = exp(-lam/scale * scale) underflows -> log-domain path
+        log_mode = !(std::exp((-lam / scale) * scale) > 0.0);
+    } else {
+        gmax = 0.0;  // E = 1 * (0 - (-log K)) = log K
+        coef = 1.0;
+    }
+    SkPlan plan = sk_plan<T>(n, h.num_sms);
+    SkArgs a{};
+    a.G = Gin; a.ld = c.ld; a.n = n;
+    a.f[0] = h.f[0].as<double>(); a.f[1] = h.f[1].as<double>();
+    a.g[0] = h.g[0].as<double>(); a.g[1] = h.g[1].as<double>();
+    a.colpart = h.colpart.p; a.ldp = ld_for(n);
+    a.devpart = h.devpart.as<double>(); a.devcol = h.devcol.as<double>();
+    a.st = h.state.as<SkState>(); a.nblk = plan.nblk;
+    GOAT_CUDA(cudaMemsetAsync(a.f[0], 0, c.ld * 8, c.s));
+    GOAT_CUDA(cudaMemsetAsync(a.g[0], 0, c.ld * 8, c.s));
+    SkState st0{};
+    st0.k = log_mode ? 1 : 0;
+    st0.gmax = gmax; st0.coef = coef; st0.tol = tol; st0.max_sweeps = max_sweeps; st0.log_mode = log_mode;
+    *h.h_state = st0;
+    GOAT_CUDA(cudaMemcpyAsync(a.st, h.h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
+    const int max_passes = max_sweeps + 2;
+    const int poll = 8;
+    for (int p = 0; p < max_passes; ++p) {
+        sk_launch_pass<T>(a, plan, c.s);
+        sk_launch_merge<T>(a, plan, c.s);
+        if ((p + 1) % poll == 0 || p + 1 == max_passes) {
+            GOAT_CUDA(cudaMemcpyAsync(h.h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost, c.s));
+            sync(c);
+            if (h.h_state->done) break;
+        }
+    }
+    GOAT_CUDA(cudaMemcpyAsync(h.h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    if (!h.h_state->done) throw Error(GOAT_ECUDA, "sinkhorn loop did not terminate");
+    out.sweeps = h.h_state->sweeps;
+    out.converged = h.h_state->converged;
+    out.dev = h.h_state->dev;
+    double *part = h.red.as<double>();
+    const int eb = kRedBlocks;
+    sk_launch_emit<T>(a, Q, c.ld, P, c.ld, L, c.ld, part, eb, c.s);
+    if (P || L) {
+        // reuse the 5-wide finisher on [nrm, lq, *, *] rows of width 4 -> do it on host
+        std::vector<double> hp((size_t)eb * 4);
+        GOAT_CUDA(cudaMemcpyAsync(hp.data(), part, eb * 4 * 8, cudaMemcpyDeviceToHost, c.s));
+        sync(c);
+        double nrm = 0, lq = 0;
+        for (int b = 0; b < eb; ++b) { nrm += hp[b * 4]; lq += hp[b * 4 + 1]; }
+        out.nrm = nrm;
+        out.lq = lq;
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------ LAP
+template <class T>
+int run_lap(Ctx &c, const T *M, int sense, int *perm_dev, std::vector<int> &perm_host) {
+    Handle &h = c.h;
+    const int n = c.n;
+    int *cand = perm_dev;
+    int *hits = h.lap_i[3].as<int>();
+    int *flag = h.lap_misc.as<int>();
+    launch_lap_certificate<T>(M, c.ld, n, sense, cand, hits, flag, c.s);
+    int certified = 0;
+    GOAT_CUDA(cudaMemcpyAsync(&certified, flag, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    if (!certified) {
+        LapWork w{};
+        w.u = h.lap_d[0].as<double>(); w.v = h.lap_d[1].as<double>(); w.spc = h.lap_d[2].as<double>();
+        w.path = h.lap_i[0].as<int>(); w.row4col = h.lap_i[1].as<int>();
+        w.col4row = perm_dev; w.rem = h.lap_i[2].as<int>();
+        w.SR = h.lap_b[0].as<unsigned char>(); w.SC = h.lap_b[1].as<unsigned char>();
+        w.status = flag + 4;
+        launch_lap_sap<T>(M, c.ld, n, sense, w, c.s);
+        int status = 0;
+        GOAT_CUDA(cudaMemcpyAsync(&status, w.status, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+        sync(c);
+        if (status != 0) throw Error(GOAT_EINVAL, "cost matrix is infeasible");
+    }
+    perm_host.resize(n);
+    GOAT_CUDA(cudaMemcpyAsync(perm_host.data(), perm_dev, n * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    return certified;
+}
+
+double alpha_opt(double c2, double c1, int sense) {
+    // matcher.py:125-135
+    if (c2 != 0.0) {
+        const double crit = -c1 / (2.0 * c2);
+        const bool ok = (sense == GOAT_MAXIMIZE) ? (c2 < 0) : (c2 > 0);
+        if (ok && 0.0 <= crit && crit <= 1.0) return crit;
+    }
+    const double end = c2 + c1;
+    if (sense == GOAT_MAXIMIZE) return end >= 0.0 ? 1.0 : 0.0;
+    return end <= 0.0 ? 1.0 : 0.0;
+}
+
+struct Timer {
+    cudaEvent_t a, b;
+    cudaStream_t s;
+    explicit Timer(cudaStream_t st) : s(st) {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+    }
+    double stop() {
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        return ms;
+    }
+    ~Timer() { cudaEventDestroy(a); cudaEventDestroy(b); }
+};
+
+// Core loop on device-resident inputs in the workspace (A, B, optional L, P = P0).
+template <class T>
+void fw_loop(Ctx &c, bool have_L, bool p0_bary, const goat_options &o, goat_fw_result *res) {
+    Handle &h = c.h;
+    const int n = c.n;
+    const int64_t ld = c.ld;
+    T *A = h.A.as<T>(), *B = h.B.as<T>();
+    T *P = h.P.as<T>(), *Q = h.Q.as<T>(), *G = h.G.as<T>(), *GQ = h.GQ.as<T>(), *T1 = h.T1.as<T>();
+    T *L = have_L ? h.L.as<T>() : nullptr;
+    T *Gl = have_L ? h.Gl.as<T>() : nullptr;
+    double *dots = h.scal.as<double>() + 16;
+    double *hd = h.h_scal + 16;
+    double t_grad = 0, t_lot = 0, t_ls = 0, t_lap = 0;
+
+    c.sym = is_symmetric<T>(c, A) && is_symmetric<T>(c, B);
+    {
+        Timer tm(c.s);
+        if (p0_bary) {
+            launch_fill<T>(P, ld, n, 1.0 / n, c.s);  // core.py:89-93
+            launch_bary_grad<T>(A, ld, B, ld, G, ld, n, h.vec.as<double>(), c.s);
+        } else {
+            gradient<T>(c, A, B, P, G, T1);
+        }
+        t_grad += tm.stop();
+    }
+    // f(P0) (matcher.py:184): <G(P0), P0>/2 + <L, P0>
+    launch_fw_dots<T>(G, G, P, P, L, ld, n, h.red.as<double>(), dots, c.s);
+    GOAT_CUDA(cudaMemcpyAsync(hd, dots, 6 * 8, cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    res->hist_obj[0] = 0.5 * hd[2] + (have_L ? hd[5] : 0.0);
+    res->hist_alpha[0] = NAN;
+    int iterations = 0, converged = 0;
+    for (int i = 1; i <= o.max_iters; ++i) {
+        const T *Gin = G;
+        if (have_L) { launch_add<T>(G, L, Gl, ld, n, c.s); Gin = Gl; }
+        LotOut lo;
+        {
+            Timer tm(c.s);
+            if (o.step_solver == GOAT_STEP_LOT) {
+                lo = run_lot<T>(c, Gin, o.sense, o.lam, o.max_sweeps, o.sk_tol, Q, nullptr, nullptr, 0);
+            } else {
+                // FAQ step (matcher.py:191-192): Q = permutation_matrix(LAP(G))
+                std::vector<int> ph;
+                run_lap<T>(c, Gin, o.sense, h.ivec.as<int>(), ph);
+                launch_perm_matrix<T>(h.ivec.as<int>(), Q, ld, n, c.s);
+                lo.sweeps = 0; lo.converged = 1;
+            }
+            t_lot += tm.stop();
+        }
+        if (res->lot_sweeps) res->lot_sweeps[i - 1] = lo.sweeps;
+        if (res->lot_converged) res->lot_converged[i - 1] = lo.converged;
+        if (res->lot_dev) res->lot_dev[i - 1] = lo.dev;
+        {
+            Timer tm(c.s);
+            gradient<T>(c, A, B, Q, GQ, T1);
+            t_grad += tm.stop();
+        }
+        Timer tm(c.s);
+        launch_fw_dots<T>(G, GQ, P, Q, L, ld, n, h.red.as<double>(), dots, c.s);
+        GOAT_CUDA(cudaMemcpyAsync(hd, dots, 6 * 8, cudaMemcpyDeviceToHost, c.s));
+        sync(c);
+        // g(a) = f(Q + a D) = f(Q) + c1 a + c2 a^2, D = P - Q (matcher.py:110-122)
+        const double c1 = hd[0] + (have_L ? hd[4] : 0.0);
+        const double c2 = 0.5 * hd[1];
+        const double fQ = 0.5 * hd[2] + (have_L ? hd[5] : 0.0);
+        const double nrm = hd[3];
+        const double al = alpha_opt(c2, c1, o.sense);
+        const double bl = 1.0 - al;
+        res->hist_obj[i] = fQ + al * c1 + al * al * c2;  // f(aP + (1-a)Q)
+        res->hist_alpha[i] = al;
+        const double step = std::fabs(bl) * std::sqrt(nrm);  // ||P_new - P||_F
+        if (al == 0.0) {
+            std::swap(h.P.p, h.Q.p);
+            std::swap(h.G.p, h.GQ.p);
+            P = h.P.as<T>(); Q = h.Q.as<T>(); G = h.G.as<T>(); GQ = h.GQ.as<T>();
+        } else if (al != 1.0) {
+            launch_axpby<T>(bl, Q, al, P, ld, n, c.s);   // P <- a P + (1-a) Q
+            launch_axpby<T>(bl, GQ, al, G, ld, n, c.s);  // G <- a G + (1-a) G(Q)
+        }
+        iterations = i;
+        t_ls += tm.stop();
+        if (step < o.fw_tol) { converged = 1; break; }
+    }
+    // final projection (matcher.py:205-211)
+    const T *Gin = G;
+    if (have_L) { launch_add<T>(G, L, Gl, ld, n, c.s); Gin = Gl; }
+    std::vector<int> ph;
+    Timer tm(c.s);
+    res->lap_certified = run_lap<T>(c, Gin, o.sense, h.ivec.as<int>(), ph);
+    t_lap += tm.stop();
+    for (int r = 0; r < n; ++r) res->assignment[r] = ph[r];
+    res->iterations = iterations;
+    res->converged = converged;
+    res->time_ms[0] = t_grad; res->time_ms[1] = t_lot; res->time_ms[2] = t_ls; res->time_ms[3] = t_lap;
+}
+
+template <class T>
+void objective_on_device(Ctx &c, bool have64) {
+    Handle &h = c.h;
+    if (!have64) {
+        ensure_f64_inputs(h, c.n);
+        launch_convert_to_f64<T>(h.A.as<T>(), c.ld, h.A64.as<double>(), c.ld, c.n, c.s);
+        launch_convert_to_f64<T>(h.B.as<T>(), c.ld, h.B64.as<double>(), c.ld, c.n, c.s);
+    }
+}
+
+void validate_opts(const goat_options *o) {
+    require(o != nullptr, "options must not be NULL");
+    require(o->max_iters >= 1, "max_iters must be at least 1");
+    require(o->fw_tol > 0, "fw_tol must be positive");
+    require(o->lam > 0, "lam must be positive");
+    require(o->max_sweeps >= 1, "max_sweeps must be at least 1");
+    require(o->sk_tol > 0, "tol must be positive");
+    require(o->sense == GOAT_MINIMIZE || o->sense == GOAT_MAXIMIZE, "bad objective sense");
+    require(o->step_solver == GOAT_STEP_LOT || o->step_solver == GOAT_STEP_EXACT_LAP, "bad step_solver");
+}
+
+template <class T>
+void fw_core_host(Handle &h, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb,
+                  const double *L, int64_t ldl, const double *P0, int64_t ldp, const goat_options *o,
+                  goat_fw_result *res) {
+    auto t0 = std::chrono::steady_clock::now();
+    ensure_workspace(h, n);
+    ensure_f64_inputs(h, n);
+    if (L) { h.L.ensure(h.A.bytes); h.Gl.ensure(h.A.bytes); }
+    Ctx c(h, (int)n);
+    Timer setup(c.s);
+    upload<T>(c, A, lda, h.A.as<T>(), h.A64.as<double>());
+    upload<T>(c, B, ldb, h.B.as<T>(), h.B64.as<double>());
+    if (L) upload<T>(c, L, ldl, h.L.as<T>(), h.stage.as<double>());
+    if (P0) upload<T>(c, P0, ldp, h.P.as<T>(), h.stage.as<double>());
+    res->time_ms[4] = setup.stop();
+    fw_loop<T>(c, L != nullptr, P0 == nullptr, *o, res);
+    // objective on the inputs (core.py:120-124), fp64, fixed order
+    int *perm = h.ivec.as<int>();
+    std::vector<int> ph(n);
+    for (int64_t r = 0; r < n; ++r) ph[r] = (int)res->assignment[r];
+    GOAT_CUDA(cudaMemcpyAsync(perm, ph.data(), n * 4, cudaMemcpyHostToDevice, c.s));
+    launch_qap_perm(h.A64.as<double>(), c.ld, h.B64.as<double>(), c.ld, perm, (int)n, h.red.as<double>(),
+                    h.scal.as<double>() + 40, c.s);
+    GOAT_CUDA(cudaMemcpyAsync(h.h_scal + 40, h.scal.as<double>() + 40, 8, cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    res->objective = h.h_scal[40];
+    res->time_ms[5] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+template <class T>
+void fw_core_dev(Handle &h, int64_t n, const T *A, int64_t lda, const T *B, int64_t ldb, const T *L,
+                 int64_t ldl, const T *P0, int64_t ldp, const goat_options *o, goat_fw_result *res) {
+    auto t0 = std::chrono::steady_clock::now();
+    ensure_workspace(h, n);
+    if (L) { h.L.ensure(h.A.bytes); h.Gl.ensure(h.A.bytes); }
+    Ctx c(h, (int)n);
+    const size_t es = sizeof(T);
+    auto cp = [&](const T *src, int64_t lds, T *dst) {
+        GOAT_CUDA(cudaMemcpy2DAsync(dst, c.ld * es, src, lds * es, n * es, n, cudaMemcpyDeviceToDevice, c.s));
+    };
+    GOAT_CUDA(cudaMemsetAsync(h.A.p, 0, h.A.bytes, c.s));
+    GOAT_CUDA(cudaMemsetAsync(h.B.p, 0, h.B.bytes, c.s));
+    cp(A, lda, h.A.as<T>());
+    cp(B, ldb, h.B.as<T>());
+    if (L) cp(L, ldl, h.L.as<T>());
+    if (P0) cp(P0, ldp, h.P.as<T>());
+    res->time_ms[4] = 0;
+    fw_loop<T>(c, L != nullptr, P0 == nullptr, *o, res);
+    ensure_f64_inputs(h, n);
+    objective_on_device<T>(c, false);
+    int *perm = h.ivec.as<int>();
+    std::vector<int> ph(n);
+    for (int64_t r = 0; r < n; ++r) ph[r] = (int)res->assignment[r];
+    GOAT_CUDA(cudaMemcpyAsync(perm, ph.data(), n * 4, cudaMemcpyHostToDevice, c.s));
+    launch_qap_perm(h.A64.as<double>(), c.ld, h.B64.as<double>(), c.ld, perm, (int)n, h.red.as<double>(),
+                    h.scal.as<double>() + 40, c.s);
+    GOAT_CUDA(cudaMemcpyAsync(h.h_scal + 40, h.scal.as<double>() + 40, 8, cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    res->objective = h.h_scal[40];
+    res->time_ms[5] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+template <class F> int guarded(F &&f) {
+    try {
+        f();
+        return GOAT_OK;
+    } catch (const Error &e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return GOAT_ECUDA;
+    }
+}
+
+void check_order(int64_t n) {
+    require(n >= 1, "order must be positive");
+    require(n <= (int64_t)1 << 30, "order too large");
+}
+
+template <class F> void dispatch(Handle &h, F &&f) {
+    if (h.precision == GOAT_FP32) f((float *)nullptr);
+    else f((double *)nullptr);
+}
+
+}  // namespace
+}  // namespace goat
+
+using namespace goat;
+
+struct goat_handle : goat::Handle {};
+
+extern "C" {
+
+const char *goat_last_error(void) { return g_last_error.c_str(); }
+
+const char *goat_version(void) { return "goat 0.1 sm_100a (fused log-domain sinkhorn, device LSAP)"; }
+
+int goat_create(goat_handle **out, const goat_config *cfg) {
+    return guarded([&] {
+        require(out != nullptr, "out must not be NULL");
+        goat_config def{0, GOAT_FP64, GOAT_GEMM_AUTO, 3};
+        const goat_config &c = cfg ? *cfg : def;
+        require(c.precision == GOAT_FP32 || c.precision == GOAT_FP64, "precision must be GOAT_FP32 or GOAT_FP64");
+        int count = 0;
+        GOAT_CUDA(cudaGetDeviceCount(&count));
+        require(c.device >= 0 && c.device < count, "device ordinal out of range");
+        auto *h = new goat_handle();
+        h->device = c.device;
+        h->precision = c.precision;
+        h->gemm = c.gemm;
+        h->split = c.split_terms ? c.split_terms : 3;
+        try {
+            GOAT_CUDA(cudaSetDevice(c.device));
+            GOAT_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, c.device));
+            GOAT_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+            h->stream = h->own_stream;
+            GOAT_CUDA(cudaMallocHost(&h->h_scal, 64 * sizeof(double)));
+            GOAT_CUDA(cudaMallocHost(&h->h_state, sizeof(SkState)));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int goat_destroy(goat_handle *h) {
+    return guarded([&] {
+        if (!h) return;
+        cudaSetDevice(h->device);
+        cudaStreamSynchronize(h->stream);
+        delete h;
+    });
+}
+
+int goat_reserve(goat_handle *h, int64_t n) {
+    return guarded([&] {
+        require(h != nullptr, "handle must not be NULL");
+        check_order(n);
+        ensure_workspace(*h, n);
+    });
+}
+
+int goat_fw_core(goat_handle *h, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb,
+                 const double *L, int64_t ldl, const double *P0, int64_t ldp, const goat_options *opts,
+                 goat_fw_result *res) {
+    return guarded([&] {
+        require(h && A && B && res && res->assignment && res->hist_obj && res->hist_alpha, "NULL argument");
+        check_order(n);
+        validate_opts(opts);
+        require(lda >= n && ldb >= n && (!L || ldl >= n) && (!P0 || ldp >= n), "leading dimension < n");
+        launch_count() = 0;
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            fw_core_host<T>(*h, n, A, lda, B, ldb, L, ldl, P0, ldp, opts, res);
+        });
+        res->gpu_launches = (int32_t)launch_count();
+    });
+}
+
+int goat_fw_core_device(goat_handle *h, int64_t n, const void *dA, int64_t lda, const void *dB, int64_t ldb,
+                        const void *dL, int64_t ldl, const void *dP0, int64_t ldp, const goat_options *opts,
+                        goat_fw_result *res) {
+    return guarded([&] {
+        require(h && dA && dB && res && res->assignment && res->hist_obj && res->hist_alpha, "NULL argument");
+        check_order(n);
+        validate_opts(opts);
+        require(lda >= n && ldb >= n && (!dL || ldl >= n) && (!dP0 || ldp >= n), "leading dimension < n");
+        launch_count() = 0;
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            fw_core_dev<T>(*h, n, (const T *)dA, lda, (const T *)dB, ldb, (const T *)dL, ldl, (const T *)dP0, ldp,
+                           opts, res);
+        });
+        res->gpu_launches = (int32_t)launch_count();
+    });
+}
+
+int goat_gradient(goat_handle *h, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb,
+                  const double *P, int64_t ldp, double *G, int64_t ldg) {
+    return guarded([&] {
+        require(h && A && B && P && G, "NULL argument");
+        check_order(n);
+        ensure_workspace(*h, n);
+        ensure_f64_inputs(*h, n);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            Ctx c(*h, (int)n);
+            double *stage = h->stage.as<double>();
+            upload<T>(c, A, lda, h->A.as<T>(), stage);
+            upload<T>(c, B, ldb, h->B.as<T>(), stage);
+            upload<T>(c, P, ldp, h->P.as<T>(), stage);
+            c.sym = is_symmetric<T>(c, h->A.as<T>()) && is_symmetric<T>(c, h->B.as<T>());
+            gradient<T>(c, h->A.as<T>(), h->B.as<T>(), h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());
+            download<T>(c, h->G.as<T>(), G, ldg, stage);
+        });
+    });
+}
+
+static int lot_common(goat_handle *h, int64_t n, const double *M, int64_t ldm, int32_t sense, double lam,
+                      int32_t max_sweeps, double tol, double *Q, int64_t ldq, int32_t *converged,
+                      int32_t *sweeps, double *deviation, int mode) {
+    return guarded([&] {
+        require(h && M && Q, "NULL argument");
+        check_order(n);
+        require(sense == GOAT_MINIMIZE || sense == GOAT_MAXIMIZE, "sense must be minimize or maximize");
+        require(lam > 0 && max_sweeps >= 1 && tol > 0, "invalid Sinkhorn parameters");
+        ensure_workspace(*h, n);
+        ensure_f64_inputs(*h, n);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            Ctx c(*h, (int)n);
+            double *stage = h->stage.as<double>();
+            upload<T>(c, M, ldm, h->M.as<T>(), stage);
+            const T *Gin = h->M.as<T>();
+            if (mode == 1) {
+                int *bad = h->ivec.as<int>();
+                GOAT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.s));
+                launch_neglog<T>(h->M.as<T>(), c.ld, h->G.as<T>(), c.ld, (int)n, bad, c.s);
+                int hb = 0;
+                GOAT_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+                sync(c);
+                require(!hb, "sinkhorn_knopp requires strictly positive entries");
+                Gin = h->G.as<T>();
+            }
+            LotOut lo = run_lot<T>(c, Gin, sense, lam, max_sweeps, tol, h->Q.as<T>(), nullptr, nullptr, mode);
+            if (converged) *converged = lo.converged;
+            if (sweeps) *sweeps = lo.sweeps;
+            if (deviation) *deviation = lo.dev;
+            if (mode == 1 && lo.sweeps == 0) {  // sinkhorn.py:71-72 returns K itself
+                for (int64_t r = 0; r < n; ++r) std::memcpy(Q + r * ldq, M + r * ldm, n * 8);
+            } else {
+                download<T>(c, h->Q.as<T>(), Q, ldq, stage);
+            }
+        });
+    });
+}
+
+int goat_lot(goat_handle *h, int64_t n, const double *M, int64_t ldm, int32_t sense, double lam,
+             int32_t max_sweeps, double tol, double *Q, int64_t ldq, int32_t *converged, int32_t *sweeps,
+             double *deviation) {
+    return lot_common(h, n, M, ldm, sense, lam, max_sweeps, tol, Q, ldq, converged, sweeps, deviation, 0);
+}
+
+int goat_sinkhorn_knopp(goat_handle *h, int64_t n, const double *K, int64_t ldk, int32_t max_sweeps, double tol,
+                        double *Q, int64_t ldq, int32_t *converged, int32_t *sweeps, double *deviation) {
+    return lot_common(h, n, K, ldk, GOAT_MAXIMIZE, 1.0, max_sweeps, tol, Q, ldq, converged, sweeps, deviation, 1);
+}
+
+int goat_line_search_coeffs(goat_handle *h, int64_t n, const double *A, int64_t lda, const double *B,
+                            int64_t ldb, const double *L, int64_t ldl, const double *P, int64_t ldp,
+                            const double *Q, int64_t ldq, double *c2, double *c1) {
+    return guarded([&] {
+        require(h && A && B && P && Q && c2 && c1, "NULL argument");
+        check_order(n);
+        ensure_workspace(*h, n);
+        ensure_f64_inputs(*h, n);
+        if (L) h->L.ensure(h->A.bytes);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            Ctx c(*h, (int)n);
+            double *stage = h->stage.as<double>();
+            upload<T>(c, A, lda, h->A.as<T>(), stage);
+            upload<T>(c, B, ldb, h->B.as<T>(), stage);
+            upload<T>(c, P, ldp, h->P.as<T>(), stage);
+            upload<T>(c, Q, ldq, h->Q.as<T>(), stage);
+            T *Ld = nullptr;
+            if (L) { upload<T>(c, L, ldl, h->L.as<T>(), stage); Ld = h->L.as<T>(); }
+            c.sym = is_symmetric<T>(c, h->A.as<T>()) && is_symmetric<T>(c, h->B.as<T>());
+            gradient<T>(c, h->A.as<T>(), h->B.as<T>(), h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());
+            gradient<T>(c, h->A.as<T>(), h->B.as<T>(), h->Q.as<T>(), h->GQ.as<T>(), h->T1.as<T>());
+            double *d = h->scal.as<double>() + 16;
+            launch_fw_dots<T>(h->G.as<T>(), h->GQ.as<T>(), h->P.as<T>(), h->Q.as<T>(), Ld, c.ld, (int)n,
+                              h->red.as<double>(), d, c.s);
+            GOAT_CUDA(cudaMemcpyAsync(h->h_scal + 16, d, 6 * 8, cudaMemcpyDeviceToHost, c.s));
+            sync(c);
+            *c2 = 0.5 * h->h_scal[17];
+            *c1 = h->h_scal[16] + (L ? h->h_scal[20] : 0.0);
+        });
+    });
+}
+
+int goat_set_stream(goat_handle *h, void *stream) {
+    return guarded([&] {
+        require(h != nullptr, "handle must not be NULL");
+        h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
+    });
+}
+
+int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int32_t reps, double *ms_per_sweep) {
+    return guarded([&] {
+        require(h && dG && ms_per_sweep && reps >= 1, "bad argument");
+        check_order(n);
+        ensure_workspace(*h, n);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            Ctx c(*h, (int)n);
+            SkPlan plan = sk_plan<T>((int)n, h->num_sms);
+            SkArgs a{};
+            a.G = dG; a.ld = ld; a.n = (int)n;
+            a.f[0] = h->f[0].as<double>(); a.f[1] = h->f[1].as<double>();
+            a.g[0] = h->g[0].as<double>(); a.g[1] = h->g[1].as<double>();
+            a.colpart = h->colpart.p; a.ldp = ld_for(n);
+            a.devpart = h->devpart.as<double>(); a.devcol = h->devcol.as<double>();
+            a.st = h->state.as<SkState>(); a.nblk = plan.nblk;
+            GOAT_CUDA(cudaMemsetAsync(h->f[0].p, 0, c.ld * 8, c.s));
+            GOAT_CUDA(cudaMemsetAsync(h->f[1].p, 0, c.ld * 8, c.s));
+            GOAT_CUDA(cudaMemsetAsync(h->g[0].p, 0, c.ld * 8, c.s));
+            GOAT_CUDA(cudaMemsetAsync(h->g[1].p, 0, c.ld * 8, c.s));
+            SkState st{};
+            st.k = 5;  // a regular mid-run sweep (row + column phases)
+            st.gmax = 0.0; st.coef = -1.0; st.tol = 1e-8; st.max_sweeps = 1000;
+            *h->h_state = st;
+            GOAT_CUDA(cudaMemcpyAsync(a.st, h->h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
+            sk_launch_pass<T>(a, plan, c.s);  // warm
+            cudaEvent_t e0, e1;
+            GOAT_CUDA(cudaEventCreate(&e0));
+            GOAT_CUDA(cudaEventCreate(&e1));
+            GOAT_CUDA(cudaEventRecord(e0, c.s));
+            for (int r = 0; r < reps; ++r) sk_launch_pass<T>(a, plan, c.s);
+            GOAT_CUDA(cudaEventRecord(e1, c.s));
+            GOAT_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            GOAT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            *ms_per_sweep = ms / reps;
+        });
+    });
+}
+
+int goat_lap(goat_handle *h, int64_t n, const double *M, int64_t ldm, int32_t sense, int64_t *assignment,
+             double *objective, int32_t *certified) {
+    return guarded([&] {
+        require(h && M && assignment, "NULL argument");
+        check_order(n);
+        require(sense == GOAT_MINIMIZE || sense == GOAT_MAXIMIZE, "sense must be minimize or maximize");
+        ensure_workspace(*h, n);
+        ensure_f64_inputs(*h, n);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            Ctx c(*h, (int)n);
+            upload<T>(c, M, ldm, h->M.as<T>(), h->stage.as<double>());
+            std::vector<int> ph;
+            const int cert = run_lap<T>(c, h->M.as<T>(), sense, h->ivec.as<int>(), ph);
+            if (certified) *certified = cert;
+            double obj = 0.0;
+            for (int64_t r = 0; r < n; ++r) {
+                assignment[r] = ph[r];
+                obj += M[r * ldm + ph[r]];
+            }
+            if (objective) *objective = obj;
+        });
+    });
+}
+
+int goat_qap_objective_perm(goat_handle *h, int64_t n, const double *A, int64_t lda, const double *B,
+                            int64_t ldb, const int64_t *perm, double *objective) {
+    return guarded([&] {
+        require(h && A && B && perm && objective, "NULL argument");
+        check_order(n);
+        ensure_workspace(*h, n);
+        ensure_f64_inputs(*h, n);
+        std::vector<int> ph(n);
+        std::vector<char> seen(n, 0);
+        for (int64_t r = 0; r < n; ++r) {
+            require(perm[r] >= 0 && perm[r] < n && !seen[perm[r]], "permutation is not a bijection");
+            seen[perm[r]] = 1;
+            ph[r] = (int)perm[r];
+        }
+        Ctx c(*h, (int)n);
+        GOAT_CUDA(cudaMemcpy2DAsync(h->A64.p, c.ld * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, c.s));
+        GOAT_CUDA(cudaMemcpy2DAsync(h->B64.p, c.ld * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, c.s));
+        int *pd = h->ivec.as<int>();
+        GOAT_CUDA(cudaMemcpyAsync(pd, ph.data(), n * 4, cudaMemcpyHostToDevice, c.s));
+        launch_qap_perm(h->A64.as<double>(), c.ld, h->B64.as<double>(), c.ld, pd, (int)n, h->red.as<double>(),
+                        h->scal.as<double>() + 40, c.s);
+        GOAT_CUDA(cudaMemcpyAsync(h->h_scal + 40, h->scal.as<double>() + 40, 8, cudaMemcpyDeviceToHost, c.s));
+        sync(c);
+        *objective = h->h_scal[40];
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// Launchers shared between the C-ABI layer and the kernel translation units.
+#pragma once
+
+#include "common.cuh"
+
+namespace goat {
+
+// ---------------------------------------------------------------- Sinkhorn
+// Log-domain Sinkhorn on E_ij = coef * (gmax - G_ij) (sinkhorn.py:115-126),
+// with the exact sweep semantics of sinkhorn_knopp (sinkhorn.py:60-85).
+struct SkArgs {
+    const void *G;      // n x n, element type = precision, leading dim ld
+    int64_t ld;
+    int n;
+    double *f[2];       // row potentials, ring of 2 (fp64)
+    double *g[2];       // column potentials, ring of 2 (fp64)
+    void *colpart;      // [nblk][ldp] per-CTA column partial sums (element type)
+    int64_t ldp;
+    double *devpart;    // [nblk] per-CTA max row deviation
+    double *devcol;     // [merge blocks] max column deviation (pre-check)
+    SkState *st;
+    int nblk;           // CTAs of the pass kernel
+};
+
+struct SkPlan {
+    int ch = 0;        // 16-byte chunks per thread
+    int rows = 0;      // rows per band
+    int nblk = 0;      // pass-kernel CTAs
+    int merge_blocks = 0;
+    size_t colpart_bytes = 0;
+};
+
+template <class T> SkPlan sk_plan(int n, int num_sms);
+template <class T> void sk_launch_pass(const SkArgs &a, const SkPlan &p, cudaStream_t s);
+template <class T> void sk_launch_merge(const SkArgs &a, const SkPlan &p, cudaStream_t s);
+// Q = exp(E + f + g) for the returned slot; optional fused partial sums:
+// part[blk*4 + 0] = sum (Q-P)^2, [1] = <L,Q>.  P, L may be null.
+template <class T>
+void sk_launch_emit(const SkArgs &a, T *Q, int64_t ldq, const T *P, int64_t ldp, const T *L,
+                    int64_t ldl, double *part, int nblk, cudaStream_t s);
+
+// ---------------------------------------------------------------- reductions
+// Deterministic two-stage reductions (fixed grid, fixed order).
+constexpr int kRedBlocks = 296;
+template <class T>
+void launch_minmax(const T *X, int64_t ld, int n, double *part, double *out2, cudaStream_t s);
+// D = P - Q: out[0]=<GQ,D>, [1]=<GP-GQ,D>, [2]=<GQ,Q>, [3]=|D|^2, [4]=<L,D>, [5]=<L,Q>
+template <class T>
+void launch_fw_dots(const T *GP, const T *GQ, const T *P, const T *Q, const T *L, int64_t ld, int n,
+                    double *part, double *out6, cudaStream_t s);
+// out[0] = sum_ij A_ij * B_{p(i)p(j)}  (A, B fp64)
+void launch_qap_perm(const double *A, int64_t lda, const double *B, int64_t ldb,
+                     const int *perm, int n, double *part, double *out, cudaStream_t s);
+template <class T>
+void launch_convert(const double *src, int64_t lds, T *dst, int64_t ldd, int n, double scale,
+                    cudaStream_t s);
+template <class T>
+void launch_convert_to_f64(const T *src, int64_t lds, double *dst, int64_t ldd, int n,
+                           cudaStream_t s);
+template <class T> void launch_fill(T *dst, int64_t ld, int n, double value, cudaStream_t s);
+// Y = a*X + b*Y  (elementwise, matcher.py:197)
+template <class T>
+void launch_axpby(double a, const T *X, double b, T *Y, int64_t ld, int n, cudaStream_t s);
+// Q = permutation matrix of perm (core.py:64-70)
+template <class T> void launch_perm_matrix(const int *perm, T *Q, int64_t ld, int n, cudaStream_t s);
+// Y = X + L
+template <class T>
+void launch_add(const T *X, const T *L, T *Y, int64_t ld, int n, cudaStream_t s);
+// G_ij = (ra_i rb_j + ca_i cb_j) / n  (gradient at the barycenter, rank 2)
+template <class T>
+void launch_bary_grad(const T *A, int64_t lda, const T *B, int64_t ldb, T *G, int64_t ldg,
+                      int n, double *vec4n, cudaStream_t s);
+// 1 if X == X^T exactly, written to *flag (int)
+template <class T>
+void launch_is_symmetric(const T *X, int64_t ld, int n, int *flag, cudaStream_t s);
+// Y = -log(X) (sinkhorn_knopp entry); *bad set to 1 if any X <= 0
+template <class T>
+void launch_neglog(const T *X, int64_t ldx, T *Y, int64_t ldy, int n, int *bad, cudaStream_t s);
+
+// ---------------------------------------------------------------- GEMM
+// C = alpha * op(A) op(B) + beta * C, op = transpose when trans != 0 (SIMT).
+template <class T>
+void gemm_simt(int m, int n, int k, double alpha, const T *A, int64_t lda, int transA,
+               const T *B, int64_t ldb, int transB, double beta, T *C, int64_t ldc,
+               cudaStream_t s);
+
+// ---------------------------------------------------------------- LAP
+// Certificate: strict row-argmax (sense-aware) forming a permutation.
+template <class T>
+void launch_lap_certificate(const T *M, int64_t ld, int n, int sense, int *cand, int *hits,
+                            int *flag, cudaStream_t s);
+// Exact shortest-augmenting-path LSAP with scipy's visiting order (lap.cu).
+struct LapWork {
+    double *u, *v, *spc;
+    int *path, *row4col, *col4row, *rem;
+    unsigned char *SR, *SC;
+    int *status;
+};
+template <class T>
+void launch_lap_sap(const T *M, int64_t ld, int n, int sense, const LapWork &w, cudaStream_t s);
+
+}  // namespace goat

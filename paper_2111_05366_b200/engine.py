@@ -1,0 +1,159 @@
+"""Frank-Wolfe graph matching entry points (drop-in for otmatch's engine).
+
+``frank_wolfe_match`` / ``seeded_match`` keep the reference's signatures,
+options and results (matcher.py:298-310).  The host keeps exactly the
+bookkeeping the reference does around its Frank-Wolfe core -- input
+validation, seed reordering, per-restart numpy RNG streams
+``default_rng([rng_seed, r])``, input shuffling, the seeded linear term and
+the best-of-restarts choice (matcher.py:230-295) -- so the random streams and
+relabelings are identical; the core itself (matcher.py:177-212: gradient,
+LOT, exact line search, update, final LAP) runs on the device in one
+``goat_fw_core`` call.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _lib
+from .matrices import as_square_matrix, invert_permutation, permute_matrix, qap_objective
+from .ops import randomized_blend_init
+from .records import MatchOptions, MatchResult, SeedSet
+
+__all__ = ["frank_wolfe_match", "seeded_match", "fw_core"]
+
+
+def fw_core(A, B, L, P0, opts: MatchOptions):
+    """Device Frank-Wolfe core: the replacement for ``_fw_core`` (matcher.py:177-212).
+
+    ``P0=None`` means the barycenter.  Returns (assignment, history, iterations,
+    converged, diagnostics).
+    """
+    n = A.shape[0]
+    h = _lib.handle(opts.device, opts.precision)
+    A_ = _lib.f64(A)
+    B_ = _lib.f64(B)
+    L_ = _lib.f64(L) if L is not None else None
+    P_ = _lib.f64(P0) if P0 is not None else None
+    mi = opts.max_iters
+    assign = np.empty(n, dtype=np.int64)
+    hobj = np.empty(mi + 1)
+    halpha = np.empty(mi + 1)
+    sweeps = np.zeros(mi, dtype=np.int32)
+    lconv = np.zeros(mi, dtype=np.int32)
+    ldev = np.zeros(mi)
+    res = _lib.GoatFwResult()
+    res.assignment = assign.ctypes.data_as(_lib._c_i64_p)
+    res.hist_obj = _lib.dptr(hobj)
+    res.hist_alpha = _lib.dptr(halpha)
+    res.lot_sweeps = sweeps.ctypes.data_as(_lib._c_i32_p)
+    res.lot_converged = lconv.ctypes.data_as(_lib._c_i32_p)
+    res.lot_dev = _lib.dptr(ldev)
+    o = _lib.GoatOptions(
+        max_iters=mi, max_sweeps=opts.sinkhorn.max_sweeps,
+        sense=_lib.GOAT_MAXIMIZE if opts.objective_sense == "maximize" else _lib.GOAT_MINIMIZE,
+        step_solver=_lib.GOAT_STEP_LOT if opts.step_solver == "lot" else _lib.GOAT_STEP_EXACT_LAP,
+        fw_tol=opts.fw_tol, lam=opts.sinkhorn.lam, sk_tol=opts.sinkhorn.tol)
+    lib = _lib.load()
+    with h.lock:
+        _lib.check(lib.goat_fw_core(
+            h.ptr, n, _lib.dptr(A_), _lib.ld_of(A_), _lib.dptr(B_), _lib.ld_of(B_),
+            _lib.dptr(L_) if L_ is not None else None, _lib.ld_of(L_) if L_ is not None else n,
+            _lib.dptr(P_) if P_ is not None else None, _lib.ld_of(P_) if P_ is not None else n,
+            o, res))
+    it = int(res.iterations)
+    history = [(0, float(hobj[0]), None)]
+    history += [(i, float(hobj[i]), float(halpha[i])) for i in range(1, it + 1)]
+    diag = dict(lot_sweeps=sweeps[:it].tolist(), lot_converged=lconv[:it].astype(bool).tolist(),
+                lot_deviation=ldev[:it].tolist(), lap_certified=bool(res.lap_certified),
+                gpu_launches=int(res.gpu_launches), objective=float(res.objective),
+                time_ms=dict(zip(("gradient", "lot", "line_search", "lap", "setup", "total"),
+                                 list(res.time_ms))))
+    return assign.astype(np.intp), history, it, bool(res.converged), diag
+
+
+def _initial(n, opts: MatchOptions, rng):
+    # matcher.py:215-223; None = barycenter (the device forms it on the fly)
+    if isinstance(opts.init, str):
+        if opts.init == "barycenter":
+            return None
+        return randomized_blend_init(n, rng, device=opts.device)
+    P0 = as_square_matrix(opts.init, "init")
+    if P0.shape[0] != n:
+        raise ValueError(f"supplied init has order {P0.shape[0]}, expected {n}")
+    return P0
+
+
+def _quadratic_1x1(A22, B22, L):
+    val = float(A22[0, 0] * B22[0, 0])
+    return val + (float(L[0, 0]) if L is not None else 0.0)
+
+
+def _match(A, B, pairs: np.ndarray, opts: MatchOptions) -> MatchResult:
+    t0 = time.perf_counter()
+    A = as_square_matrix(A, "A")
+    B = as_square_matrix(B, "B")
+    if A.shape != B.shape:
+        raise ValueError(f"order mismatch: {A.shape[0]} vs {B.shape[0]}")
+    n = A.shape[0]
+    m = pairs.shape[0]
+    if m >= n:
+        raise ValueError(f"seed count {m} must be less than order {n}")
+    if m and (pairs.min() < 0 or pairs.max() >= n):
+        raise ValueError("seed vertex out of range")
+    # seeds first, identity-aligned at [0, m) (matcher.py:244-250)
+    rest1 = np.setdiff1d(np.arange(n), pairs[:, 0]) if m else np.arange(n)
+    rest2 = np.setdiff1d(np.arange(n), pairs[:, 1]) if m else np.arange(n)
+    ord1 = np.concatenate([pairs[:, 0], rest1]).astype(np.intp)
+    ord2 = np.concatenate([pairs[:, 1], rest2]).astype(np.intp)
+    Ar = A[np.ix_(ord1, ord1)] if m else A
+    Br = B[np.ix_(ord2, ord2)] if m else B
+    nf = n - m
+    best = None
+    for r in range(opts.n_restarts):
+        rng = np.random.default_rng([opts.rng_seed, r])
+        if opts.shuffle_input and nf > 1:
+            shuf = rng.permutation(nf).astype(np.intp)
+        else:
+            shuf = np.arange(nf, dtype=np.intp)
+        inv = invert_permutation(shuf)
+        B22 = permute_matrix(Br[m:, m:], shuf) if opts.shuffle_input else Br[m:, m:]
+        A22 = Ar[m:, m:]
+        L = None
+        if m:
+            B12 = Br[:m, m:][:, inv]
+            B21 = Br[m:, :m][inv, :]
+            L = Ar[m:, :m] @ B21.T + Ar[:m, m:].T @ B12  # constant seed term (matcher.py:267)
+        diag = None
+        if nf == 1:
+            p22 = np.zeros(1, dtype=np.intp)
+            history, iters, conv = [(0, _quadratic_1x1(A22, B22, L), None)], 0, True
+        else:
+            P0 = _initial(nf, opts, rng)
+            p22, history, iters, conv, diag = fw_core(A22, B22, L, P0, opts)
+        p22 = inv[p22]
+        align = np.empty(n, dtype=np.intp)
+        align[ord1[:m]] = ord2[:m]
+        align[ord1[m:]] = ord2[m + p22]
+        if m == 0 and diag is not None:
+            # same terms A_ij B_{align(i) align(j)}, already reduced on the device
+            obj = diag["objective"]
+        else:
+            obj = qap_objective(A, B, align, device=opts.device)
+        if best is None or (obj > best[1] if opts.objective_sense == "maximize" else obj < best[1]):
+            best = (align, obj, iters, history, conv, diag)
+    align, obj, iters, history, conv, diag = best
+    return MatchResult(alignment=align, objective=obj, iterations=iters, iterate_history=history,
+                       converged=conv, wall_time=time.perf_counter() - t0, diagnostics=diag)
+
+
+def frank_wolfe_match(A, B, opts: MatchOptions = MatchOptions()) -> MatchResult:
+    """Match two equal-order graphs; FAQ or GOAT depending on ``opts.step_solver``."""
+    return _match(A, B, np.empty((0, 2), dtype=np.intp), opts)
+
+
+def seeded_match(A, B, seeds: SeedSet, opts: MatchOptions = MatchOptions()) -> MatchResult:
+    """Match with seed pairs pinned; Frank-Wolfe over the free block only."""
+    return _match(A, B, seeds.pairs, opts)
