@@ -184,20 +184,28 @@ def run_ours(args):
     dB = torch.from_numpy(B.astype(np.float32)).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2
 
+    phases = {}
+
     def device_step():
         mi = opts.max_iters
         assign = np.empty(n, dtype=np.int64)
         hobj = np.empty(mi + 1)
         halpha = np.empty(mi + 1)
+        sweeps = np.zeros(mi, dtype=np.int32)
         res = _lib.GoatFwResult()
         res.assignment = assign.ctypes.data_as(_lib._c_i64_p)
         res.hist_obj = _lib.dptr(hobj)
         res.hist_alpha = _lib.dptr(halpha)
+        res.lot_sweeps = sweeps.ctypes.data_as(_lib._c_i32_p)
         o = _lib.GoatOptions(max_iters=mi, max_sweeps=1000, sense=_lib.GOAT_MAXIMIZE,
                              step_solver=_lib.GOAT_STEP_LOT, fw_tol=opts.fw_tol, lam=100.0,
                              sk_tol=1e-8)
         _lib.check(lib.goat_fw_core_device(h.ptr, n, dA.data_ptr(), n, dB.data_ptr(), n, None, n,
                                            None, n, o, res))
+        phases.clear()
+        phases.update(zip(("gradient", "lot", "line_search", "lap", "setup", "total"),
+                          [round(x, 3) for x in res.time_ms]))
+        phases["lot_sweeps"] = sweeps[: int(res.iterations)].tolist()
         return int(res.iterations), int(res.gpu_launches), assign, float(res.objective)
 
     def barrier():
@@ -281,6 +289,7 @@ def run_ours(args):
                    "l2": "flushed between steps (256 MiB write); inputs 4 MB are L2-sized",
                    "iterations_per_step": iters / args.steps, "match_ratio": match,
                    "time_to_converge_ms": total_max / args.steps,
+                   "phase_ms_last_step": phases,
                    "parallelism": f"replicas x{world}"},
         "e2e": {"value": e2e_iters_all / (e2e_max / 1000.0), "unit": "iter/s",
                 "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * 8 + 8 * 2 * 31,

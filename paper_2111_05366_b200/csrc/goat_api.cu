@@ -41,7 +41,7 @@ struct Handle {
     DevBuf A, B, P, Q, G, GQ, T1, L, Gl, M;     // element = precision
     DevBuf A64, B64, stage;                     // fp64 inputs (objective) + upload staging
     DevBuf f[2], g[2], colpart, devpart, devcol, state, red, scal, vec, ivec;
-    DevBuf lap_d[3], lap_i[4], lap_b[2], lap_misc;
+    DevBuf lap_d[3], lap_i[4], lap_b[2], lap_misc, bar;
     double *h_scal = nullptr;                   // pinned host scalars
     SkState *h_state = nullptr;                 // pinned
     ~Handle() {
@@ -68,7 +68,8 @@ void ensure_workspace(Handle &h, int64_t n) {
     h.vec.ensure(vec * 4);
     h.ivec.ensure((size_t)ld * 4 * 4);
     h.devpart.ensure(4096 * 8);
-    h.devcol.ensure((size_t)(ld / kThreads + 2) * 8);
+    h.devcol.ensure((size_t)std::max<int64_t>(4096, ld / kThreads + 2) * 8);
+    h.bar.ensure(256);
     h.state.ensure(sizeof(SkState));
     h.red.ensure(kRedBlocks * 8 * 8);
     h.scal.ensure(64 * 8);
@@ -198,15 +199,19 @@ LotOut run_lot(Ctx &c, const T *Gin, int sense, double lam, int max_sweeps, doub
     st0.gmax = gmax; st0.coef = coef; st0.tol = tol; st0.max_sweeps = max_sweeps; st0.log_mode = log_mode;
     *h.h_state = st0;
     GOAT_CUDA(cudaMemcpyAsync(a.st, h.h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
-    const int max_passes = max_sweeps + 2;
-    const int poll = 8;
-    for (int p = 0; p < max_passes; ++p) {
-        sk_launch_pass<T>(a, plan, c.s);
-        sk_launch_merge<T>(a, plan, c.s);
-        if ((p + 1) % poll == 0 || p + 1 == max_passes) {
-            GOAT_CUDA(cudaMemcpyAsync(h.h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost, c.s));
-            sync(c);
-            if (h.h_state->done) break;
+    if (plan.persistent) {
+        sk_launch_persistent<T>(a, plan, h.bar.as<unsigned>(), c.s);
+    } else {
+        const int max_passes = max_sweeps + 2;
+        const int poll = 8;
+        for (int p = 0; p < max_passes; ++p) {
+            sk_launch_pass<T>(a, plan, c.s);
+            sk_launch_merge<T>(a, plan, c.s);
+            if ((p + 1) % poll == 0 || p + 1 == max_passes) {
+                GOAT_CUDA(cudaMemcpyAsync(h.h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost, c.s));
+                sync(c);
+                if (h.h_state->done) break;
+            }
         }
     }
     GOAT_CUDA(cudaMemcpyAsync(h.h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost, c.s));
@@ -719,24 +724,38 @@ int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int3
             GOAT_CUDA(cudaMemsetAsync(h->f[1].p, 0, c.ld * 8, c.s));
             GOAT_CUDA(cudaMemsetAsync(h->g[0].p, 0, c.ld * 8, c.s));
             GOAT_CUDA(cudaMemsetAsync(h->g[1].p, 0, c.ld * 8, c.s));
+            // A LOT that cannot converge (tol ~ 0): pre-check + `reps` sweeps +
+            // the row-only pass, exactly the in-situ work of the production loop.
             SkState st{};
-            st.k = 5;  // a regular mid-run sweep (row + column phases)
-            st.gmax = 0.0; st.coef = -1.0; st.tol = 1e-8; st.max_sweeps = 1000;
+            st.k = 0;
+            // E = -(100 - G) in [-100, 0] for G in [0, 100): the lam = 100 unit-range
+            // Gibbs exponent of the production loop (sinkhorn.py:125).
+            st.gmax = 100.0; st.coef = -1.0; st.tol = 1e-300; st.max_sweeps = reps;
             *h->h_state = st;
-            GOAT_CUDA(cudaMemcpyAsync(a.st, h->h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
-            sk_launch_pass<T>(a, plan, c.s);  // warm
+            auto run = [&] {
+                GOAT_CUDA(cudaMemcpyAsync(a.st, h->h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
+                if (plan.persistent) {
+                    sk_launch_persistent<T>(a, plan, h->bar.as<unsigned>(), c.s);
+                } else {
+                    for (int r = 0; r < reps + 2; ++r) {
+                        sk_launch_pass<T>(a, plan, c.s);
+                        sk_launch_merge<T>(a, plan, c.s);
+                    }
+                }
+            };
+            run();  // warm
             cudaEvent_t e0, e1;
             GOAT_CUDA(cudaEventCreate(&e0));
             GOAT_CUDA(cudaEventCreate(&e1));
             GOAT_CUDA(cudaEventRecord(e0, c.s));
-            for (int r = 0; r < reps; ++r) sk_launch_pass<T>(a, plan, c.s);
+            run();
             GOAT_CUDA(cudaEventRecord(e1, c.s));
             GOAT_CUDA(cudaEventSynchronize(e1));
             float ms = 0;
             GOAT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
-            *ms_per_sweep = ms / reps;
+            *ms_per_sweep = ms / (reps + 2);
         });
     });
 }

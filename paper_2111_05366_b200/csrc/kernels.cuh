@@ -27,12 +27,15 @@ struct SkPlan {
     int rows = 0;      // rows per band
     int nblk = 0;      // pass-kernel CTAs
     int merge_blocks = 0;
+    bool persistent = false;  // one cooperative launch for the whole sweep loop
     size_t colpart_bytes = 0;
 };
 
 template <class T> SkPlan sk_plan(int n, int num_sms);
 template <class T> void sk_launch_pass(const SkArgs &a, const SkPlan &p, cudaStream_t s);
 template <class T> void sk_launch_merge(const SkArgs &a, const SkPlan &p, cudaStream_t s);
+// All sweeps in one cooperative launch (bar: 2 unsigned of scratch).
+template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, unsigned *bar, cudaStream_t s);
 // Q = exp(E + f + g) for the returned slot; optional fused partial sums:
 // part[blk*4 + 0] = sum (Q-P)^2, [1] = <L,Q>.  P, L may be null.
 template <class T>

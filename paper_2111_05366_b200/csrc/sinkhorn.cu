@@ -9,13 +9,22 @@
 //   * row phase   f_k = -LSE_j(E_ij + g_{k-1,j})      (each CTA owns whole rows)
 //     dev_{k-1}  = max_i |expm1(f_{k-1,i} - f_{k,i})| = max|u_{k-1} K v_{k-1} - 1|
 //   * column phase, on the same registers: colpart[cta][j] = sum_i exp(E_ij + g_{k-1,j} + f_{k,i})
-// A merge kernel turns the column partials into g_k = g_{k-1} - log(sum), and its
-// last CTA applies the reference's stopping rule, so a converged loop turns every
-// later pass into a no-op without a host round trip.  Pass 0 is the reference's
-// marginal pre-check of K itself (sinkhorn.py:70-72); pass max_sweeps+1 is
-// row-only and produces the deviation of the final iterate.  The returned
-// iterate is exp(E + f_{s} + g_{s}) for the stopping sweep s -- the same u that
-// produced the reported deviation (sinkhorn.py:84-85).
+// A merge step turns the column partials into g_k = g_{k-1} - log(sum) and applies
+// the reference's stopping rule.  Pass 0 is the reference's marginal pre-check of
+// K itself (sinkhorn.py:70-72); pass max_sweeps+1 is row-only and yields the
+// deviation of the final iterate.  The returned iterate is exp(E + f_s + g_s) for
+// the stopping sweep s -- the same u that produced the reported deviation
+// (sinkhorn.py:84-85).
+//
+// Two drivers share the pass/merge bodies:
+//   * sk_persistent_kernel: ONE cooperative launch runs every sweep; CTAs meet at
+//     a software grid barrier after the pass (row results + column partials) and
+//     after the merge (new g).  Every CTA evaluates the stopping rule from the
+//     same device data, so they leave the loop together with no host round trip.
+//   * sk_pass_kernel + sk_merge_kernel: one launch pair per sweep (fallback).
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace goat {
@@ -61,65 +70,74 @@ __device__ __forceinline__ void lse_combine(T &m, T &s, T m2, T s2) {
     s = a + b;
 }
 
+// Ring slots are selected, not indexed, so SkArgs stays in the parameter bank.
+__device__ __forceinline__ double *fslot(const SkArgs &a, int s) { return (s & 1) ? a.f[1] : a.f[0]; }
+__device__ __forceinline__ double *gslot(const SkArgs &a, int s) { return (s & 1) ? a.g[1] : a.g[0]; }
+
+// ------------------------------------------------------------------ pass body
+// Rows band-cyclic over CTAs (band = blk, blk + nblk, ...), so a CTA owns the
+// same rows every pass; columns are owned per thread (16-byte chunks).
 template <class T, int CH, int R>
-__global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
+__device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
+                                          int blk, int nblk) {
     using V = typename VecT<T>::V;
     constexpr int VW = VecT<T>::W;
     constexpr int NW = kThreads / 32;
-    __shared__ int s_k, s_done;
     __shared__ T s_m[NW][R], s_s[NW][R];
     __shared__ double s_lse[R];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        s_k = *(volatile int *)&a.st->k;
-        s_done = *(volatile int *)&a.st->done;
-    }
-    __syncthreads();
-    if (s_done) return;
-    const int k = s_k;
     const int n = a.n;
     const bool pre = (k == 0);
-    const bool rowonly = (k == a.st->max_sweeps + 1);
-    // ring slots (selected, not indexed, so SkArgs stays in the constant bank)
-    const double *gin = (k & 1) ? a.g[0] : a.g[1];  // slot of g_{k-1}
-    const double *fprev = (k & 1) ? a.f[0] : a.f[1];
-    double *fout = (k & 1) ? a.f[1] : a.f[0];
+    const bool rowonly = (k == max_sweeps + 1);
+    const double *gin = gslot(a, k + 1);  // g_{k-1}
+    const double *fprev = fslot(a, k + 1);
+    double *fout = fslot(a, k);
     const T *G = static_cast<const T *>(a.G);
     const double ks = SkMath<T>::kScale;
-    const T coef = (T)(a.st->coef * ks);
-    const T gmax = (T)a.st->gmax;
+    const T coef = (T)(coef_d * ks);
+    const T gmax = (T)gmax_d;
 
-    // Per-thread columns: chunks q = tid + kThreads*c, columns q*VW .. q*VW+VW-1.
     T gl[CH][VW], acc[CH][VW];
 #pragma unroll
     for (int c = 0; c < CH; ++c)
 #pragma unroll
         for (int e = 0; e < VW; ++e) {
-            int col = (tid + kThreads * c) * VW + e;
-            gl[c][e] = (col < n && !pre) ? (T)(gin[col] * ks) : T(0);
+            const int col = (tid + kThreads * c) * VW + e;
+            gl[c][e] = (col < n && !pre) ? (T)(__ldcg(gin + col) * ks) : T(0);
             acc[c][e] = T(0);
         }
 
     double devmax = 0.0;
     const int nbands = (n + R - 1) / R;
-    for (int band = blockIdx.x; band < nbands; band += gridDim.x) {
+    // Raw 16-byte loads of one band; the next band is prefetched while the
+    // current one is reduced, so the L2/HBM latency overlaps the row combine.
+    V xv[R][CH];
+    auto load_band = [&](int band, V (&dst)[R][CH]) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int q = tid + kThreads * c;
+                const int row = band * R + r;
+                if (band < nbands && row < n && q * VW < n)
+                    dst[r][c] = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + (int64_t)q * VW));
+                else
+                    memset(&dst[r][c], 0, sizeof(V));
+            }
+    };
+    load_band(blk, xv);
+    for (int band = blk; band < nbands; band += nblk) {
         const int r0 = band * R;
         T x[R][CH][VW];
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
-                const int q = tid + kThreads * c;
-                const int row = r0 + r;
-                V v;
-                if (row < n && q * VW < n)
-                    v = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + (int64_t)q * VW));
-                else
-                    memset(&v, 0, sizeof(V));
-                const T *pv = reinterpret_cast<const T *>(&v);
+                const T *pv = reinterpret_cast<const T *>(&xv[r][c]);
 #pragma unroll
                 for (int e = 0; e < VW; ++e) x[r][c][e] = pv[e];
             }
+        load_band(band + nblk, xv);  // prefetch
         T m[R], s[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -131,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
                 for (int e = 0; e < VW; ++e) {
                     const int col = (tid + kThreads * c) * VW + e;
                     // E_ij = coef * (gmax - G_ij), reference order (sinkhorn.py:125)
-                    T arg = (rv && col < n) ? coef * (gmax - x[r][c][e]) + gl[c][e] : neg_inf<T>();
+                    const T arg = (rv && col < n) ? coef * (gmax - x[r][c][e]) + gl[c][e] : neg_inf<T>();
                     x[r][c][e] = arg;
                     m[r] = arg > m[r] ? arg : m[r];
                 }
@@ -140,8 +158,8 @@ __global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
             for (int c = 0; c < CH; ++c)
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
-                    T arg = x[r][c][e];
-                    T y = (arg == neg_inf<T>()) ? T(0) : SkMath<T>::ex(arg - m[r]);
+                    const T arg = x[r][c][e];
+                    const T y = (arg == neg_inf<T>()) ? T(0) : SkMath<T>::ex(arg - m[r]);
                     x[r][c][e] = y;
                     s[r] += y;
                 }
@@ -152,30 +170,34 @@ __global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
             T mm = m[r], ss = s[r];
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
-                T m2 = __shfl_xor_sync(0xffffffffu, mm, off);
-                T s2 = __shfl_xor_sync(0xffffffffu, ss, off);
+                const T m2 = __shfl_xor_sync(0xffffffffu, mm, off);
+                const T s2 = __shfl_xor_sync(0xffffffffu, ss, off);
                 lse_combine(mm, ss, m2, s2);
             }
             if (lane == 0) { s_m[warp][r] = mm; s_s[warp][r] = ss; }
         }
         __syncthreads();
-        if (tid < R) {
-            const int row = r0 + tid;
-            double M = -INFINITY;
-            for (int w = 0; w < NW; ++w) M = fmax(M, (double)s_m[w][tid]);
-            double S = 0.0;
-            if (M != -INFINITY)
-                for (int w = 0; w < NW; ++w)
-                    if ((double)s_m[w][tid] != -INFINITY)
-                        S += (double)s_s[w][tid] * SkMath<T>::exd((double)s_m[w][tid] - M);
-            const double lse = M + SkMath<T>::lg(S);  // scaled units
-            s_lse[tid] = lse;
+        // Cross-warp combine: warp w finishes row w (lanes 0..NW-1 hold the
+        // per-warp pairs; a fixed xor tree keeps it deterministic).
+        for (int r = warp; r < R; r += NW) {
+            T mm = lane < NW ? s_m[lane][r] : neg_inf<T>();
+            T ss = lane < NW ? s_s[lane][r] : T(0);
+#pragma unroll
+            for (int off = NW / 2; off > 0; off >>= 1) {
+                const T m2 = __shfl_xor_sync(0xffffffffu, mm, off);
+                const T s2 = __shfl_xor_sync(0xffffffffu, ss, off);
+                lse_combine(mm, ss, m2, s2);
+            }
+            if (lane != 0) continue;
+            const int row = r0 + r;
+            const double lse = (double)mm + SkMath<T>::lg((double)ss);  // scaled units
+            s_lse[r] = lse;
             if (row < n) {
                 const double fnew = -lse / ks;
                 double dev = 0.0;
-                if (pre) dev = fabs(expm1(-fnew));                 // |rowsum(K) - 1|
-                else if (k >= 2) dev = fabs(expm1(fprev[row] - fnew));  // |u K v - 1|
-                if (!pre) fout[row] = fnew;
+                if (pre) dev = fabs(expm1(-fnew));                                   // |rowsum(K) - 1|
+                else if (k >= 2) dev = fabs(expm1(__ldcg(fprev + row) - fnew));      // |u K v - 1|
+                if (!pre) __stcg(fout + row, fnew);
                 devmax = fmax(devmax, dev);
             }
         }
@@ -195,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
         }
     }
     if (!rowonly) {
-        T *cp = static_cast<T *>(a.colpart) + (int64_t)blockIdx.x * a.ldp;
+        T *cp = static_cast<T *>(a.colpart) + (int64_t)blk * a.ldp;
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
             const int q = tid + kThreads * c;
@@ -204,39 +226,190 @@ __global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
                 T *pv = reinterpret_cast<T *>(&v);
 #pragma unroll
                 for (int e = 0; e < VW; ++e) pv[e] = acc[c][e];
-                *reinterpret_cast<V *>(cp + (int64_t)q * VW) = v;
+                __stcg(reinterpret_cast<V *>(cp + (int64_t)q * VW), v);
             }
         }
     }
-    if (warp == 0) {
-        for (int off = 16; off > 0; off >>= 1) devmax = fmax(devmax, __shfl_xor_sync(0xffffffffu, devmax, off));
-        if (lane == 0) a.devpart[blockIdx.x] = devmax;
+    __shared__ double s_dev[NW];
+    if (lane == 0) s_dev[warp] = devmax;
+    __syncthreads();
+    if (tid == 0) {
+        double d = 0.0;
+        for (int w = 0; w < NW; ++w) d = fmax(d, s_dev[w]);
+        __stcg(a.devpart + blk, d);
     }
 }
 
 // Exact column LSE for a column whose partial sum under/overflowed:
 // g_j = -LSE_i(E_ij + f_i) over all rows (fp64).  Rare repair path.
 template <class T>
-__device__ double sk_exact_col(const SkArgs &a, int j, const double *f, bool pre) {
+__device__ double sk_exact_col(const SkArgs &a, int j, const double *f, bool pre, double coef, double gmax) {
     const T *G = static_cast<const T *>(a.G);
-    const double coef = a.st->coef, gmax = a.st->gmax;
     double M = -INFINITY;
     for (int i = 0; i < a.n; ++i) {
-        double e = coef * (gmax - (double)G[(int64_t)i * a.ld + j]) + (pre ? 0.0 : f[i]);
+        const double e = coef * (gmax - (double)G[(int64_t)i * a.ld + j]) + (pre ? 0.0 : __ldcg(f + i));
         M = fmax(M, e);
     }
     double S = 0.0;
     for (int i = 0; i < a.n; ++i) {
-        double e = coef * (gmax - (double)G[(int64_t)i * a.ld + j]) + (pre ? 0.0 : f[i]);
+        const double e = coef * (gmax - (double)G[(int64_t)i * a.ld + j]) + (pre ? 0.0 : __ldcg(f + i));
         S += exp(e - M);
     }
     return -(M + log(S));
 }
 
+// ------------------------------------------------------------------ merge body
+// Columns [blk*256 + tid] strided by nblk*256.  On the pre-check writes this
+// CTA's max |colsum - 1| to devcol[blk].
+template <class T>
+__device__ __forceinline__ void merge_body(const SkArgs &a, int k, double coef, double gmax, int blk, int nblk) {
+    constexpr int NW = kThreads / 32;
+    __shared__ double s_red[NW];
+    const int tid = threadIdx.x, n = a.n, lane = tid & 31, warp = tid >> 5;
+    const bool pre = (k == 0);
+    const T *cp = static_cast<const T *>(a.colpart);
+    const double tiny = sizeof(T) == 4 ? 1e-30 : 1e-290;
+    const int np = a.nblk;
+    double dloc = 0.0;
+    // One warp per column: lanes split the partials (4 independent loads in
+    // flight per lane), then a fixed xor tree -- deterministic.
+    for (int j = blk * NW + warp; j < n; j += nblk * NW) {
+        double S = 0.0;
+        for (int b0 = 0; b0 < np; b0 += 128) {
+            T v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int b = b0 + lane + 32 * u;
+                v[u] = b < np ? __ldcg(cp + (int64_t)b * a.ldp + j) : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) S += (double)v[u];
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+        if (lane != 0) continue;
+        if (pre) {
+            if (!(S > tiny)) S = exp(-sk_exact_col<T>(a, j, nullptr, true, coef, gmax));
+            dloc = fmax(dloc, fabs(S - 1.0));
+        } else {
+            const double gold = __ldcg(gslot(a, k + 1) + j);
+            double gnew = gold - log(S);
+            if (!(S > tiny) || !isfinite(S)) {
+                gnew = sk_exact_col<T>(a, j, fslot(a, k), false, coef, gmax);
+                atomicAdd(&a.st->repaired, 1);
+            }
+            __stcg(gslot(a, k) + j, gnew);
+        }
+    }
+    if (pre) {
+        for (int off = 16; off > 0; off >>= 1) dloc = fmax(dloc, __shfl_xor_sync(0xffffffffu, dloc, off));
+        if ((tid & 31) == 0) s_red[tid >> 5] = dloc;
+        __syncthreads();
+        if (tid == 0) {
+            double d = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) d = fmax(d, s_red[w]);
+            __stcg(a.devcol + blk, d);
+        }
+    }
+}
+
+// Max of cnt per-CTA values: one warp reads (coalesced), result broadcast via smem.
+__device__ __forceinline__ double max_of(const double *p, int cnt) {
+    __shared__ double s_max;
+    if (threadIdx.x < 32) {
+        double d = 0.0;
+        for (int b = threadIdx.x; b < cnt; b += 32) d = fmax(d, __ldcg(p + b));
+        for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
+        if (threadIdx.x == 0) s_max = d;
+    }
+    __syncthreads();
+    const double d = s_max;
+    __syncthreads();
+    return d;
+}
+
+// Software grid barrier for a cooperative launch: arrival counter + generation.
+// Counter and generation live on different 128-byte lines so the spinning
+// readers do not contend with the arrivals.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned *cnt = bar, *gen = bar + 32;
+        const unsigned g = ld_acquire(gen);
+        __threadfence();
+        if (atomicAdd(cnt, 1u) == nblocks - 1) {
+            atomicExch(cnt, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (ld_acquire(gen) == g) { }
+        }
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ drivers
+template <class T, int CH, int R>
+__global__ void __launch_bounds__(kThreads, 1) sk_persistent_kernel(SkArgs a, unsigned *bar) {
+    __shared__ int s_k;
+    if (threadIdx.x == 0) s_k = a.st->k;
+    __syncthreads();
+    const int k0 = s_k;
+    const int K = a.st->max_sweeps;
+    const double tol = a.st->tol, coef = a.st->coef, gmax = a.st->gmax;
+    const int blk = blockIdx.x, nblk = gridDim.x;
+    for (int k = k0;; ++k) {
+        pass_body<T, CH, R>(a, k, K, coef, gmax, blk, nblk);
+        grid_barrier(bar, nblk);
+        const double drow = max_of(a.devpart, nblk);
+        int stop = 0, sweeps = 0, conv = 0, slot = 0;
+        if (k >= 2) {
+            if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
+            else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
+        }
+        if (!stop) {
+            merge_body<T>(a, k, coef, gmax, blk, nblk);
+            grid_barrier(bar, nblk);
+            if (k == 0) {
+                const double d0 = fmax(drow, max_of(a.devcol, nblk));
+                if (d0 < tol) { stop = 1; sweeps = 0; conv = 1; slot = 0; }
+                if (blk == 0 && threadIdx.x == 0) a.st->last_dev = d0;
+                if (stop && blk == 0 && threadIdx.x == 0) a.st->dev = d0;
+            }
+        } else if (blk == 0 && threadIdx.x == 0) {
+            a.st->dev = drow;
+        }
+        if (stop) {
+            if (blk == 0 && threadIdx.x == 0) {
+                a.st->done = 1; a.st->sweeps = sweeps; a.st->converged = conv; a.st->slot = slot;
+                a.st->k = k + 1;
+            }
+            return;
+        }
+    }
+}
+
+template <class T, int CH, int R>
+__global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
+    __shared__ int s_k, s_done;
+    if (threadIdx.x == 0) {
+        s_k = *(volatile int *)&a.st->k;
+        s_done = *(volatile int *)&a.st->done;
+    }
+    __syncthreads();
+    if (s_done) return;
+    pass_body<T, CH, R>(a, s_k, a.st->max_sweeps, a.st->coef, a.st->gmax, blockIdx.x, gridDim.x);
+}
+
 template <class T>
 __global__ void __launch_bounds__(kThreads) sk_merge_kernel(SkArgs a) {
     __shared__ int s_k, s_done, s_last;
-    __shared__ double s_red[kThreads / 32];
     const int tid = threadIdx.x;
     if (tid == 0) {
         s_k = *(volatile int *)&a.st->k;
@@ -244,50 +417,24 @@ __global__ void __launch_bounds__(kThreads) sk_merge_kernel(SkArgs a) {
     }
     __syncthreads();
     if (s_done) return;
-    const int k = s_k, n = a.n;
-    const int max_sweeps = a.st->max_sweeps;
+    const int k = s_k;
+    const int K = a.st->max_sweeps;
     const double tol = a.st->tol;
     const bool pre = (k == 0);
-    const bool rowonly = (k == max_sweeps + 1);
-    const int j = blockIdx.x * kThreads + tid;
-    double dloc = 0.0;
-    if (j < n && !rowonly) {
-        const T *cp = static_cast<const T *>(a.colpart);
-        double S = 0.0;
-        for (int b = 0; b < a.nblk; ++b) S += (double)cp[(int64_t)b * a.ldp + j];
-        const double tiny = sizeof(T) == 4 ? 1e-30 : 1e-290;
-        if (pre) {
-            if (!(S > tiny)) S = exp(-sk_exact_col<T>(a, j, nullptr, true));
-            dloc = fabs(S - 1.0);
-        } else {
-            const double gold = ((k & 1) ? a.g[0] : a.g[1])[j];
-            double gnew = gold - log(S);
-            if (!(S > tiny) || !isfinite(S)) {
-                gnew = sk_exact_col<T>(a, j, (k & 1) ? a.f[1] : a.f[0], false);
-                atomicAdd(&a.st->repaired, 1);
-            }
-            ((k & 1) ? a.g[1] : a.g[0])[j] = gnew;
-        }
-    }
-    // block max of the column deviation (pre-check only)
-    for (int off = 16; off > 0; off >>= 1) dloc = fmax(dloc, __shfl_xor_sync(0xffffffffu, dloc, off));
-    if ((tid & 31) == 0) s_red[tid >> 5] = dloc;
-    __syncthreads();
+    if (k != K + 1) merge_body<T>(a, k, a.st->coef, a.st->gmax, blockIdx.x, gridDim.x);
     if (tid == 0) {
-        double d = 0.0;
-        for (int w = 0; w < kThreads / 32; ++w) d = fmax(d, s_red[w]);
-        a.devcol[blockIdx.x] = d;
+        if (!pre) __stcg(a.devcol + blockIdx.x, 0.0);
         __threadfence();
-        int t = atomicAdd(&a.st->arrive, 1);
+        const int t = atomicAdd(&a.st->arrive, 1);
         s_last = (t == (int)gridDim.x - 1);
     }
     __syncthreads();
     if (!s_last || tid != 0) return;
     __threadfence();
     // Last CTA: stopping rule of sinkhorn.py:70-72 / :82-85 (and :96-99 in log mode).
-    double drow = 0.0, dcol = 0.0;
-    for (int b = 0; b < a.nblk; ++b) drow = fmax(drow, __ldcg(&a.devpart[b]));
-    for (int b = 0; b < (int)gridDim.x; ++b) dcol = fmax(dcol, __ldcg(&a.devcol[b]));
+    double drow = 0.0, dcol = 0.0;  // single thread here
+    for (int b = 0; b < a.nblk; ++b) drow = fmax(drow, __ldcg(a.devpart + b));
+    for (int b = 0; b < (int)gridDim.x; ++b) dcol = fmax(dcol, __ldcg(a.devcol + b));
     SkState *st = a.st;
     st->arrive = 0;
     if (pre) {
@@ -305,9 +452,8 @@ __global__ void __launch_bounds__(kThreads) sk_merge_kernel(SkArgs a) {
             st->done = 1; st->sweeps = k - 1; st->converged = 1; st->slot = (k - 1) & 1; st->dev = drow;
             return;
         }
-        if (rowonly) {
-            st->done = 1; st->sweeps = max_sweeps; st->converged = 0;
-            st->slot = max_sweeps & 1; st->dev = drow;
+        if (k == K + 1) {
+            st->done = 1; st->sweeps = K; st->converged = 0; st->slot = K & 1; st->dev = drow;
             return;
         }
     }
@@ -320,25 +466,25 @@ __global__ void __launch_bounds__(kThreads) sk_emit_kernel(SkArgs a, T *Q, int64
                                                            double *part) {
     __shared__ double s_r[2][kThreads / 32];
     const int slot = a.st->slot;
-    const double *f = slot ? a.f[1] : a.f[0], *g = slot ? a.g[1] : a.g[0];
+    const double *f = fslot(a, slot), *g = gslot(a, slot);
     const T *G = static_cast<const T *>(a.G);
     const int n = a.n;
     double nrm = 0.0, lq = 0.0;
-    const float ks = (float)SkMath<float>::kScale;
     const double coef = a.st->coef, gmax = a.st->gmax;
+    const float ks = (float)SkMath<float>::kScale;
     const float coef2 = (float)(coef * SkMath<float>::kScale);
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
-        const double fi = f[i];
+        const double fi = __ldcg(f + i);
         const T *Gi = G + (int64_t)i * a.ld;
         for (int j = threadIdx.x; j < n; j += kThreads) {
             T q;
             if (sizeof(T) == 8) {
                 // exp(E + f + g), E in the reference's evaluation order
                 const double e = coef * (gmax - (double)Gi[j]);
-                q = (T)exp((e + fi) + g[j]);
+                q = (T)exp((e + fi) + __ldcg(g + j));
             } else {
                 const float e = coef2 * ((float)gmax - (float)Gi[j]);
-                q = (T)ex2f(e + (float)((fi + g[j]) * ks));
+                q = (T)ex2f(e + (float)((fi + __ldcg(g + j)) * ks));
             }
             Q[(int64_t)i * ldq + j] = q;
             if (P) { const double d = (double)q - (double)P[(int64_t)i * ldp + j]; nrm += d * d; }
@@ -359,12 +505,28 @@ __global__ void __launch_bounds__(kThreads) sk_emit_kernel(SkArgs a, T *Q, int64
     }
 }
 
-template <class T> constexpr int max_ch() { return 8; }
+constexpr int kMaxCh = 8;
 constexpr int rows_for(int ch) { return ch == 1 ? 8 : ch == 2 ? 4 : ch <= 4 ? 2 : 1; }
 
-template <class T, int CH>
-void launch_pass_ch(const SkArgs &a, const SkPlan &p, cudaStream_t s) {
-    sk_pass_kernel<T, CH, rows_for(CH)><<<p.nblk, kThreads, 0, s>>>(a); note_launch();
+template <class T, int CH> void *persistent_fn() { return (void *)sk_persistent_kernel<T, CH, rows_for(CH)>; }
+
+template <class T> void *persistent_for(int ch) {
+    switch (ch) {
+        case 1: return persistent_fn<T, 1>();
+        case 2: return persistent_fn<T, 2>();
+        case 3: return persistent_fn<T, 3>();
+        case 4: return persistent_fn<T, 4>();
+        case 5: return persistent_fn<T, 5>();
+        case 6: return persistent_fn<T, 6>();
+        case 7: return persistent_fn<T, 7>();
+        case 8: return persistent_fn<T, 8>();
+    }
+    throw Error(GOAT_ENOTSUP, "sinkhorn: bad chunk count");
+}
+
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
 }
 
 }  // namespace
@@ -374,15 +536,32 @@ template <class T> SkPlan sk_plan(int n, int num_sms) {
     SkPlan p;
     const int chunks = (n + VW - 1) / VW;
     p.ch = (chunks + kThreads - 1) / kThreads;
-    if (p.ch > max_ch<T>())
+    if (p.ch > kMaxCh)
         throw Error(GOAT_ENOTSUP, "sinkhorn: order " + std::to_string(n) +
                                       " exceeds the single-CTA row width of this build");
     p.rows = rows_for(p.ch);
     const int nbands = (n + p.rows - 1) / p.rows;
-    p.nblk = std::max(1, std::min(nbands, num_sms));
-    p.merge_blocks = (n + kThreads - 1) / kThreads;
-    p.colpart_bytes = (size_t)p.nblk * round_up(n, 8) * sizeof(T);
+    // Persistent (cooperative) driver: every CTA must be co-resident.  Fewer CTAs
+    // make the two grid barriers per sweep cheaper; aim for >= ~64 KB of G per CTA.
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)persistent_for<T>(p.ch), kThreads, 0);
+    const int coresident = std::max(1, occ) * num_sms;
+    // Measured (profiles/round1_sk_tune.json): per-sweep time falls monotonically
+    // with CTA count up to one CTA per SM at every n tested (1000..5000).
+    const int want = num_sms;
+    p.persistent = env_int("GOAT_SK_PERSISTENT", 1) != 0 && occ > 0;
+    p.nblk = std::max(1, std::min({nbands, coresident, want}));
+    if (const int force = env_int("GOAT_SK_BLOCKS", 0)) p.nblk = std::max(1, std::min({force, nbands, coresident}));
+    if (!p.persistent) p.nblk = std::max(1, std::min(nbands, num_sms));
+    p.merge_blocks = std::max(1, std::min((n + 7) / 8, 4 * num_sms));  // one warp per column
+    p.colpart_bytes = (size_t)std::max(p.nblk, num_sms * 2) * round_up(n, 8) * sizeof(T);
     return p;
+}
+
+template <class T, int CH>
+void launch_pass_ch(const SkArgs &a, const SkPlan &p, cudaStream_t s) {
+    sk_pass_kernel<T, CH, rows_for(CH)><<<p.nblk, kThreads, 0, s>>>(a);
+    note_launch();
 }
 
 template <class T> void sk_launch_pass(const SkArgs &a, const SkPlan &p, cudaStream_t s) {
@@ -405,6 +584,14 @@ template <class T> void sk_launch_merge(const SkArgs &a, const SkPlan &p, cudaSt
     GOAT_CHECK_LAUNCH();
 }
 
+template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, unsigned *bar, cudaStream_t s) {
+    GOAT_CUDA(cudaMemsetAsync(bar, 0, 64 * sizeof(unsigned), s));
+    SkArgs args = a;
+    void *params[] = {&args, &bar};
+    GOAT_CUDA(cudaLaunchCooperativeKernel(persistent_for<T>(p.ch), dim3(p.nblk), dim3(kThreads), params, 0, s));
+    note_launch();
+}
+
 template <class T>
 void sk_launch_emit(const SkArgs &a, T *Q, int64_t ldq, const T *P, int64_t ldp, const T *L,
                     int64_t ldl, double *part, int nblk, cudaStream_t s) {
@@ -418,6 +605,8 @@ template void sk_launch_pass<float>(const SkArgs &, const SkPlan &, cudaStream_t
 template void sk_launch_pass<double>(const SkArgs &, const SkPlan &, cudaStream_t);
 template void sk_launch_merge<float>(const SkArgs &, const SkPlan &, cudaStream_t);
 template void sk_launch_merge<double>(const SkArgs &, const SkPlan &, cudaStream_t);
+template void sk_launch_persistent<float>(const SkArgs &, const SkPlan &, unsigned *, cudaStream_t);
+template void sk_launch_persistent<double>(const SkArgs &, const SkPlan &, unsigned *, cudaStream_t);
 template void sk_launch_emit<float>(const SkArgs &, float *, int64_t, const float *, int64_t,
                                     const float *, int64_t, double *, int, cudaStream_t);
 template void sk_launch_emit<double>(const SkArgs &, double *, int64_t, const double *, int64_t,
