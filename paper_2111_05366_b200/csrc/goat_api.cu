@@ -17,6 +17,7 @@
 #include <cstring>
 #include <vector>
 
+#include "gemm_tc.cuh"
 #include "kernels.cuh"
 
 namespace goat {
@@ -42,6 +43,10 @@ struct Handle {
     DevBuf A64, B64, stage;                     // fp64 inputs (objective) + upload staging
     DevBuf f[2], g[2], colpart, devpart, devcol, state, red, scal, vec, ivec;
     DevBuf lap_d[3], lap_i[4], lap_b[2], lap_misc, bar;
+    // tcgen05 path: bf16 planes of A, A^T, the first-GEMM operand ([B] or [B; B^T]),
+    // the iterate X and the intermediate Y^T.
+    DevBuf tcA, tcAt, tcB, tcX, tcY, tcS;
+    int tc_na = 0, tc_nb = 0;  // planes of A / B (1 when exact in bf16)
     double *h_scal = nullptr;                   // pinned host scalars
     SkState *h_state = nullptr;                 // pinned
     ~Handle() {
@@ -96,8 +101,121 @@ struct Ctx {
     int64_t ld;
     cudaStream_t s;
     bool sym = false;
+    bool tc = false;  // gradient on tcgen05 (fp32 mode)
     Ctx(Handle &hh, int nn) : h(hh), n(nn), ld(ld_for(nn)), s(hh.stream) {}
 };
+
+// ------------------------------------------------------------------ tcgen05 gradient
+// Terms (p, q) of a split product sum_p X_p . sum_q Y_q kept when p + q < max(nx, ny):
+// drops only products of two low-order planes (below fp32 rounding).
+int add_terms(TcGemmParams &g, const __nv_bfloat16 *a, int na, int64_t a_stride, int a_rows, int a_row0,
+              const __nv_bfloat16 *b, int nb, int64_t b_stride, int b_rows, int b_row0, int64_t ld, int K) {
+    const int lim = std::max(na, nb);
+    for (int p = 0; p < na; ++p)
+        for (int q = 0; q < nb; ++q) {
+            if (p + q >= lim) continue;
+            if (g.nterms >= kTcMaxTerms) throw Error(GOAT_ENOTSUP, "tcgen05: too many split terms");
+            TcTerm &t = g.terms[g.nterms++];
+            tc_make_map(&t.a, a + p * a_stride, a_rows, K, ld, tc_box_rows_a());
+            tc_make_map(&t.b, b + q * b_stride, b_rows, K, ld, tc_box_rows_b());
+            t.a_row0 = a_row0;
+            t.b_row0 = b_row0;
+        }
+    return g.nterms;
+}
+
+// Per-solve preparation: exactness of A, B in bf16 and their planes.
+void tc_prepare(Ctx &c, const float *A, const float *B) {
+    Handle &h = c.h;
+    const int n = c.n;
+    const int64_t ld = c.ld, mat = (int64_t)n * ld;
+    int *flag = h.ivec.as<int>();
+    h.tc_na = tc_bf16_exact(A, ld, n, flag, c.s) ? 1 : h.split;
+    h.tc_nb = tc_bf16_exact(B, ld, n, flag, c.s) ? 1 : h.split;
+    const int S = h.split;
+    h.tcA.ensure(mat * 2 * h.tc_na);
+    h.tcX.ensure(mat * 2 * S);
+    const int yrows = c.sym ? n : 2 * n;
+    h.tcY.ensure((int64_t)yrows * ld * 2 * S);
+    h.tcB.ensure((int64_t)yrows * ld * 2 * h.tc_nb);
+    auto *pa = h.tcA.as<__nv_bfloat16>();
+    auto *pb = h.tcB.as<__nv_bfloat16>();
+    tc_split_planes(A, ld, n, n, pa, ld, mat, h.tc_na, c.s);
+    if (c.sym) {
+        tc_split_planes(B, ld, n, n, pb, ld, mat, h.tc_nb, c.s);  // B^T = B
+    } else {
+        h.tcAt.ensure(mat * 2 * h.tc_na);
+        tc_split_planes_t(A, ld, n, h.tcAt.as<__nv_bfloat16>(), ld, mat, h.tc_na, c.s);
+        // first-GEMM A operand, per plane: rows [0,n) = B, rows [n,2n) = B^T
+        tc_split_planes(B, ld, n, n, pb, ld, 2 * mat, h.tc_nb, c.s);
+        tc_split_planes_t(B, ld, n, pb + mat, ld, 2 * mat, h.tc_nb, c.s);
+    }
+}
+
+// out = A X B^T + A^T X B on tensor cores:
+//   Y^T = [B; B^T] X^T   (M = n or 2n)        -> bf16 planes of Y^T
+//   G   = A Y1 + A^T Y2  (K-concatenated)     -> fp32
+void tc_gradient(Ctx &c, const float *X, float *out) {
+    Handle &h = c.h;
+    const int n = c.n, S = h.split;
+    const int64_t ld = c.ld, mat = (int64_t)n * ld;
+    const int yrows = c.sym ? n : 2 * n;
+    auto *px = h.tcX.as<__nv_bfloat16>();
+    auto *py = h.tcY.as<__nv_bfloat16>();
+    tc_split_planes(X, ld, n, n, px, ld, mat, S, c.s);
+    const int64_t ystride = (int64_t)yrows * ld;
+    const int kblocks = ceil_div(n, tc_block_k());
+    // Split-K: the tensor core's fp32 accumulation error grows with the number of
+    // chained MMAs, so the K range is cut into slices reduced in fixed order with
+    // round-to-nearest adds; slices also fill the SMs when there are few tiles.
+    // Steps per slice: <= 2 (term, k-block) steps when workspace allows (measured:
+    // error ~1e-6 of max|G| at n<=3000), at most 16 slices, <= 2 GiB of slices.
+    auto set_slices = [&](TcGemmParams &g, int rows) {
+        const int steps = g.nterms * kblocks;
+        int sl = std::min(16, ceil_div(steps, 2));
+        if (const char *e = getenv("GOAT_TC_KSLICES")) sl = std::max(1, atoi(e));
+        const int64_t cap = (int64_t)1 << 31;
+        while (sl > 1 && (int64_t)sl * rows * ld * 4 > cap) --sl;
+        sl = std::max(1, std::min(sl, steps));
+        g.kpb = ceil_div(steps, sl);
+        g.kslices = ceil_div(steps, g.kpb);
+    };
+    static thread_local TcGemmParams g1, g2;
+    // Y^T = [B; B^T] X^T
+    g1.nterms = 0;
+    add_terms(g1, h.tcB.as<__nv_bfloat16>(), h.tc_nb, ystride, yrows, 0, px, S, mat, n, 0, ld, n);
+    g1.M = yrows; g1.N = n; g1.K = n; g1.kblocks = kblocks; g1.alpha = 1.f;
+    set_slices(g1, yrows);
+    if (g1.kslices == 1) {
+        g1.mode = 1; g1.planes = py; g1.ldpl = ld; g1.plane_stride = ystride; g1.nplanes = S;
+        g1.C = nullptr; g1.ldc = 0; g1.slice_stride = 0;
+        tc_gemm(g1, c.s);
+    } else {
+        h.tcS.ensure((size_t)g1.kslices * ystride * 4);
+        g1.mode = 0; g1.C = h.tcS.as<float>(); g1.ldc = ld; g1.slice_stride = ystride;
+        g1.planes = nullptr; g1.nplanes = 0;
+        tc_gemm(g1, c.s);
+        tc_slice_reduce(h.tcS.as<float>(), ystride, g1.kslices, yrows, n, ld, 1.f, nullptr, py, ystride, S, c.s);
+    }
+    // G = A Y1 (+ A^T Y2)
+    g2.nterms = 0;
+    add_terms(g2, h.tcA.as<__nv_bfloat16>(), h.tc_na, mat, n, 0, py, S, ystride, yrows, 0, ld, n);
+    if (!c.sym)
+        add_terms(g2, h.tcAt.as<__nv_bfloat16>(), h.tc_na, mat, n, 0, py, S, ystride, yrows, n, ld, n);
+    const float alpha = c.sym ? 2.f : 1.f;
+    g2.M = n; g2.N = n; g2.K = n; g2.kblocks = kblocks;
+    set_slices(g2, n);
+    g2.mode = 0; g2.planes = nullptr; g2.nplanes = 0; g2.ldc = ld;
+    if (g2.kslices == 1) {
+        g2.alpha = alpha; g2.C = out; g2.slice_stride = 0;
+        tc_gemm(g2, c.s);
+    } else {
+        h.tcS.ensure((size_t)g2.kslices * mat * 4);
+        g2.alpha = 1.f; g2.C = h.tcS.as<float>(); g2.slice_stride = mat;
+        tc_gemm(g2, c.s);
+        tc_slice_reduce(h.tcS.as<float>(), mat, g2.kslices, n, n, ld, alpha, out, nullptr, 0, 0, c.s);
+    }
+}
 
 // Upload a host fp64 matrix (leading dim lds) into dst (precision T, ld).
 template <class T>
@@ -122,6 +240,12 @@ template <class T>
 void gradient(Ctx &c, const T *A, const T *B, const T *X, T *out, T *tmp) {
     const int n = c.n;
     const int64_t ld = c.ld;
+    if constexpr (std::is_same<T, float>::value) {
+        if (c.tc) {
+            tc_gradient(c, X, out);
+            return;
+        }
+    }
     if (c.sym) {
         gemm_simt<T>(n, n, n, 1.0, X, ld, 0, B, ld, 0, 0.0, tmp, ld, c.s);
         gemm_simt<T>(n, n, n, 2.0, A, ld, 0, tmp, ld, 0, 0.0, out, ld, c.s);
@@ -130,6 +254,14 @@ void gradient(Ctx &c, const T *A, const T *B, const T *X, T *out, T *tmp) {
         gemm_simt<T>(n, n, n, 1.0, A, ld, 0, tmp, ld, 0, 0.0, out, ld, c.s);  // A (X B^T)
         gemm_simt<T>(n, n, n, 1.0, X, ld, 0, B, ld, 0, 0.0, tmp, ld, c.s);  // X B
         gemm_simt<T>(n, n, n, 1.0, A, ld, 1, tmp, ld, 0, 1.0, out, ld, c.s);  // + A^T (X B)
+    }
+}
+
+// Engine choice: fp32 runs the gradient on tcgen05 unless GOAT_GEMM_SIMT was asked for.
+template <class T> void setup_gemm(Ctx &c, const T *A, const T *B) {
+    if constexpr (std::is_same<T, float>::value) {
+        c.tc = c.h.gemm != GOAT_GEMM_SIMT;
+        if (c.tc) tc_prepare(c, A, B);
     }
 }
 
@@ -312,6 +444,7 @@ void fw_loop(Ctx &c, bool have_L, bool p0_bary, const goat_options &o, goat_fw_r
     double t_grad = 0, t_lot = 0, t_ls = 0, t_lap = 0;
 
     c.sym = is_symmetric<T>(c, A) && is_symmetric<T>(c, B);
+    setup_gemm<T>(c, A, B);
     {
         Timer tm(c.s);
         if (p0_bary) {
@@ -608,6 +741,7 @@ int goat_gradient(goat_handle *h, int64_t n, const double *A, int64_t lda, const
             upload<T>(c, B, ldb, h->B.as<T>(), stage);
             upload<T>(c, P, ldp, h->P.as<T>(), stage);
             c.sym = is_symmetric<T>(c, h->A.as<T>()) && is_symmetric<T>(c, h->B.as<T>());
+            setup_gemm<T>(c, h->A.as<T>(), h->B.as<T>());
             gradient<T>(c, h->A.as<T>(), h->B.as<T>(), h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());
             download<T>(c, h->G.as<T>(), G, ldg, stage);
         });
@@ -684,6 +818,7 @@ int goat_line_search_coeffs(goat_handle *h, int64_t n, const double *A, int64_t 
             T *Ld = nullptr;
             if (L) { upload<T>(c, L, ldl, h->L.as<T>(), stage); Ld = h->L.as<T>(); }
             c.sym = is_symmetric<T>(c, h->A.as<T>()) && is_symmetric<T>(c, h->B.as<T>());
+            setup_gemm<T>(c, h->A.as<T>(), h->B.as<T>());
             gradient<T>(c, h->A.as<T>(), h->B.as<T>(), h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());
             gradient<T>(c, h->A.as<T>(), h->B.as<T>(), h->Q.as<T>(), h->GQ.as<T>(), h->T1.as<T>());
             double *d = h->scal.as<double>() + 16;

@@ -1,6 +1,6 @@
 # usage: bash scripts/gpu_check.sh [pytest-args]
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
-timeout 900 python -m pytest tests/test_parity_gpu.py -q -m gpu --timeout 600 -p no:cacheprovider "$@" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -40 gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests/ -q -m gpu --timeout 600 -p no:cacheprovider "$@" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+grep -E "passed|failed|Error|error" gpurun_out/pytest_gpu.log | tail -25
 timeout 600 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
-tail -5 gpurun_out/bench.log
+tail -3 gpurun_out/bench.log

@@ -48,3 +48,12 @@ def test_library_is_sm100a_only(lib_path):
                          text=True).stdout
     archs = set(re.findall(r"sm_(\d+a?)", out))
     assert archs == {"100a"}, archs
+
+
+def test_tensor_core_path_is_tcgen05(lib_path):
+    """The fp32 gradient GEMM must be tcgen05/TMA/TMEM (not mma.sync/wmma)."""
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib_path], capture_output=True,
+                         text=True).stdout
+    for mnemonic in ("UTCHMMA", "UTMALDG", "LDTM"):
+        assert mnemonic in out, mnemonic
+    assert "HMMA" not in out.replace("UTCHMMA", "")
