@@ -74,7 +74,7 @@ void ensure_workspace(Handle &h, int64_t n) {
     h.ivec.ensure((size_t)ld * 4 * 4);
     h.devpart.ensure(4096 * 8);
     h.devcol.ensure((size_t)std::max<int64_t>(4096, ld / kThreads + 2) * 8);
-    h.bar.ensure(256);
+    h.bar.ensure(1024);
     h.state.ensure(sizeof(SkState));
     h.red.ensure(kRedBlocks * 8 * 8);
     h.scal.ensure(64 * 8);

@@ -20,6 +20,7 @@ struct SkArgs {
     double *devcol;     // [merge blocks] max column deviation (pre-check)
     SkState *st;
     int nblk;           // CTAs of the pass kernel
+    unsigned long long *dslot = nullptr;  // persistent driver: atomicMax dev slots [row k&1 | col]
 };
 
 struct SkPlan {

@@ -46,13 +46,18 @@ template <> struct SkMath<float> {
     static constexpr double kScale = 1.4426950408889634;  // log2(e)
     __device__ static float ex(float x) { return ex2f(x); }
     __device__ static double lg(double x) { return log2(x); }
+    __device__ static double lgt(float x) { return (double)__log2f(x); }  // SFU log2
     __device__ static double exd(double x) { return exp2(x); }
+    // |expm1(d)| at fp32 resolution (fp32 mode cannot resolve below ~1e-7 anyway)
+    __device__ static double dev(double d) { return (double)fabsf(expm1f((float)d)); }
 };
 template <> struct SkMath<double> {
     static constexpr double kScale = 1.0;
     __device__ static double ex(double x) { return exp(x); }
     __device__ static double lg(double x) { return log(x); }
+    __device__ static double lgt(double x) { return log(x); }
     __device__ static double exd(double x) { return exp(x); }
+    __device__ static double dev(double d) { return fabs(expm1(d)); }
 };
 
 template <class T> __device__ __forceinline__ T neg_inf();
@@ -83,8 +88,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
     using V = typename VecT<T>::V;
     constexpr int VW = VecT<T>::W;
     constexpr int NW = kThreads / 32;
-    __shared__ T s_m[NW][R], s_s[NW][R];
-    __shared__ double s_lse[R];
+    __shared__ T s_m[2][NW][R], s_s[2][NW][R];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = a.n;
     const bool pre = (k == 0);
@@ -138,6 +142,9 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
                 for (int e = 0; e < VW; ++e) x[r][c][e] = pv[e];
             }
         load_band(band + nblk, xv);  // prefetch
+        // f_{k-1} of row r0 + lane (warp 0 checks the deviation), fetched early
+        double fprev_v = 0.0;
+        if (warp == 0 && lane < R && k >= 2 && r0 + lane < n) fprev_v = __ldcg(fprev + r0 + lane);
         T m[R], s[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -153,6 +160,18 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
                     x[r][c][e] = arg;
                     m[r] = arg > m[r] ? arg : m[r];
                 }
+        }
+        // Warp max first (shuffle + max only), then exponentials against the warp
+        // max and a plain sum butterfly: no SFU op on the shuffle chain.
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const T m2 = __shfl_xor_sync(0xffffffffu, m[r], off);
+                m[r] = m2 > m[r] ? m2 : m[r];
+            }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
             s[r] = T(0);
 #pragma unroll
             for (int c = 0; c < CH; ++c)
@@ -164,50 +183,51 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
                     s[r] += y;
                 }
         }
-        // Block-wide (m, s) combine per row: warp shuffles, then smem across warps.
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            T mm = m[r], ss = s[r];
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const T m2 = __shfl_xor_sync(0xffffffffu, mm, off);
-                const T s2 = __shfl_xor_sync(0xffffffffu, ss, off);
-                lse_combine(mm, ss, m2, s2);
-            }
-            if (lane == 0) { s_m[warp][r] = mm; s_s[warp][r] = ss; }
+            for (int off = 16; off > 0; off >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], off);
+        }
+        // Per-warp pairs into a parity-double-buffered slot: one block barrier per
+        // band; every warp then finishes all R rows itself (lane r <- row r) in
+        // the same fixed order, so the results agree bit-for-bit across warps.
+        const int par = ((band - blk) / nblk) & 1;
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) { s_m[par][warp][r] = m[r]; s_s[par][warp][r] = s[r]; }
         }
         __syncthreads();
-        // Cross-warp combine: warp w finishes row w (lanes 0..NW-1 hold the
-        // per-warp pairs; a fixed xor tree keeps it deterministic).
-        for (int r = warp; r < R; r += NW) {
-            T mm = lane < NW ? s_m[lane][r] : neg_inf<T>();
-            T ss = lane < NW ? s_s[lane][r] : T(0);
+        double lse_l = 0.0;
+        if (lane < R) {
+            T M = neg_inf<T>();
 #pragma unroll
-            for (int off = NW / 2; off > 0; off >>= 1) {
-                const T m2 = __shfl_xor_sync(0xffffffffu, mm, off);
-                const T s2 = __shfl_xor_sync(0xffffffffu, ss, off);
-                lse_combine(mm, ss, m2, s2);
+            for (int w = 0; w < NW; ++w) { const T mw = s_m[par][w][lane]; M = mw > M ? mw : M; }
+            T S = T(0);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const T mw = s_m[par][w][lane];
+                if (mw != neg_inf<T>()) S += s_s[par][w][lane] * SkMath<T>::ex(mw - M);
             }
-            if (lane != 0) continue;
-            const int row = r0 + r;
-            const double lse = (double)mm + SkMath<T>::lg((double)ss);  // scaled units
-            s_lse[r] = lse;
-            if (row < n) {
-                const double fnew = -lse / ks;
+            lse_l = (double)M + SkMath<T>::lgt(S);  // scaled units
+            const int row = r0 + lane;
+            if (warp == 0 && row < n) {
+                const double fnew = -lse_l / ks;
                 double dev = 0.0;
-                if (pre) dev = fabs(expm1(-fnew));                                   // |rowsum(K) - 1|
-                else if (k >= 2) dev = fabs(expm1(__ldcg(fprev + row) - fnew));      // |u K v - 1|
+                if (pre) dev = SkMath<T>::dev(-fnew);                  // |rowsum(K) - 1|
+                else if (k >= 2) dev = SkMath<T>::dev(fprev_v - fnew);  // |u K v - 1|
                 if (!pre) __stcg(fout + row, fnew);
                 devmax = fmax(devmax, dev);
             }
         }
-        __syncthreads();
+        double lse_r[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) lse_r[r] = __shfl_sync(0xffffffffu, lse_l, r);
         if (!rowonly) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 if (m[r] == neg_inf<T>()) continue;
                 // column contribution y = x * exp(m + f_col), f_col = 0 on the pre-check
-                const double colf = pre ? 0.0 : -s_lse[r];
+                const double colf = pre ? 0.0 : -lse_r[r];
                 const T sc = SkMath<T>::ex((T)((double)m[r] + colf));
 #pragma unroll
                 for (int c = 0; c < CH; ++c)
@@ -231,12 +251,17 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         }
     }
     __shared__ double s_dev[NW];
+    // rows are finished by lanes 0..R-1: reduce over the whole warp first
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) devmax = fmax(devmax, __shfl_xor_sync(0xffffffffu, devmax, off));
     if (lane == 0) s_dev[warp] = devmax;
     __syncthreads();
     if (tid == 0) {
         double d = 0.0;
         for (int w = 0; w < NW; ++w) d = fmax(d, s_dev[w]);
         __stcg(a.devpart + blk, d);
+        // max of non-negative doubles == max of their bit patterns: order-independent
+        if (a.dslot) atomicMax(a.dslot + (k & 1), (unsigned long long)__double_as_longlong(d));
     }
 }
 
@@ -309,6 +334,7 @@ __device__ __forceinline__ void merge_body(const SkArgs &a, int k, double coef, 
             double d = 0.0;
             for (int w = 0; w < kThreads / 32; ++w) d = fmax(d, s_red[w]);
             __stcg(a.devcol + blk, d);
+            if (a.dslot) atomicMax(a.dslot + 2, (unsigned long long)__double_as_longlong(d));
         }
     }
 }
@@ -337,26 +363,23 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     return v;
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
+// Monotone arrival counter (zeroed per launch): arrival is a release reduction,
+// waiting is acquire polling until epoch * nblocks.  Measured 1.2 us at 148
+// CTAs vs 2.0 us for a fence + generation-flag barrier (scripts/barrier_bench.cu).
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks, unsigned &epoch) {
+    ++epoch;
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned *cnt = bar, *gen = bar + 32;
-        const unsigned g = ld_acquire(gen);
-        __threadfence();
-        if (atomicAdd(cnt, 1u) == nblocks - 1) {
-            atomicExch(cnt, 0u);
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            while (ld_acquire(gen) == g) { }
-        }
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(bar), "r"(1u) : "memory");
+        const unsigned target = epoch * nblocks;
+        while (ld_acquire(bar) < target) { }
     }
     __syncthreads();
 }
 
 // ------------------------------------------------------------------ drivers
 template <class T, int CH, int R>
-__global__ void __launch_bounds__(kThreads, 1) sk_persistent_kernel(SkArgs a, unsigned *bar) {
+__global__ void __launch_bounds__(kThreads, 2) sk_persistent_kernel(SkArgs a, unsigned *bar) {
     __shared__ int s_k;
     if (threadIdx.x == 0) s_k = a.st->k;
     __syncthreads();
@@ -364,10 +387,12 @@ __global__ void __launch_bounds__(kThreads, 1) sk_persistent_kernel(SkArgs a, un
     const int K = a.st->max_sweeps;
     const double tol = a.st->tol, coef = a.st->coef, gmax = a.st->gmax;
     const int blk = blockIdx.x, nblk = gridDim.x;
+    unsigned epoch = 0;
     for (int k = k0;; ++k) {
         pass_body<T, CH, R>(a, k, K, coef, gmax, blk, nblk);
-        grid_barrier(bar, nblk);
-        const double drow = max_of(a.devpart, nblk);
+        grid_barrier(bar, nblk, epoch);
+        const double drow = __longlong_as_double((long long)__ldcg(a.dslot + (k & 1)));
+        if (blk == 0 && threadIdx.x == 0) a.dslot[(k + 1) & 1] = 0ull;  // next sweep's slot
         int stop = 0, sweeps = 0, conv = 0, slot = 0;
         if (k >= 2) {
             if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
@@ -375,9 +400,9 @@ __global__ void __launch_bounds__(kThreads, 1) sk_persistent_kernel(SkArgs a, un
         }
         if (!stop) {
             merge_body<T>(a, k, coef, gmax, blk, nblk);
-            grid_barrier(bar, nblk);
+            grid_barrier(bar, nblk, epoch);
             if (k == 0) {
-                const double d0 = fmax(drow, max_of(a.devcol, nblk));
+                const double d0 = fmax(drow, __longlong_as_double((long long)__ldcg(a.dslot + 2)));
                 if (d0 < tol) { stop = 1; sweeps = 0; conv = 1; slot = 0; }
                 if (blk == 0 && threadIdx.x == 0) a.st->last_dev = d0;
                 if (stop && blk == 0 && threadIdx.x == 0) a.st->dev = d0;
@@ -548,7 +573,7 @@ template <class T> SkPlan sk_plan(int n, int num_sms) {
     const int coresident = std::max(1, occ) * num_sms;
     // Measured (profiles/round1_sk_tune.json): per-sweep time falls monotonically
     // with CTA count up to one CTA per SM at every n tested (1000..5000).
-    const int want = num_sms;
+    const int want = coresident;
     p.persistent = env_int("GOAT_SK_PERSISTENT", 1) != 0 && occ > 0;
     p.nblk = std::max(1, std::min({nbands, coresident, want}));
     if (const int force = env_int("GOAT_SK_BLOCKS", 0)) p.nblk = std::max(1, std::min({force, nbands, coresident}));
@@ -585,8 +610,10 @@ template <class T> void sk_launch_merge(const SkArgs &a, const SkPlan &p, cudaSt
 }
 
 template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, unsigned *bar, cudaStream_t s) {
-    GOAT_CUDA(cudaMemsetAsync(bar, 0, 64 * sizeof(unsigned), s));
+    // bar: [0] arrivals, [32] generation, bytes [512, 544) the dev-max slots
+    GOAT_CUDA(cudaMemsetAsync(bar, 0, 1024, s));
     SkArgs args = a;
+    args.dslot = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(bar) + 512);
     void *params[] = {&args, &bar};
     GOAT_CUDA(cudaLaunchCooperativeKernel(persistent_for<T>(p.ch), dim3(p.nblk), dim3(kThreads), params, 0, s));
     note_launch();

