@@ -263,6 +263,7 @@ def run_ours(args):
     bytes_per_sweep = n * n * 4
     achieved = bytes_per_sweep / (msw * 1e-3) / 1e9
     peak, peak_kind = _peaks()
+    kernels = _kernel_scan(lib, h, dev, peak)
 
     if world > 1:
         t = torch.tensor([total_ms, float(iters), sum(e2e_ms), float(e2e_iters)], dtype=torch.float64, device=dev)
@@ -300,6 +301,7 @@ def run_ours(args):
                      "note": f"{bytes_per_sweep} algorithmic bytes/launch (n^2 fp32, one read of G); "
                              f"{msw * 1000:.2f} us/launch; at n=1000 G is L2-resident"},
         "cpu_baseline": {k: v for k, v in cpu.items()},
+        "kernels": kernels,
         "clocks": clocks.summary(),
         "gpu_launches": launches,
     }
@@ -319,6 +321,53 @@ def _ms_per_sweep(lib, h, n, G):
     out = ctypes.c_double()
     _lib.check(lib.goat_bench_sweep(h.ptr, n, G.data_ptr(), n, 200, ctypes.byref(out)))
     return out.value
+
+
+def _bf16_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 1590.0, "fallback"
+
+
+def _kernel_scan(lib, h, dev, hbm_peak):
+    """Per-kernel rates at the other BASELINE sizes (context for the metric's
+    'Sinkhorn HBM GB/s; GEMM TFLOP/s' parts; not the headline)."""
+    import ctypes
+    import torch
+    from paper_2111_05366_b200 import _lib
+    out = {}
+    tf_peak, tf_kind = _bf16_peak()
+    for n in (2000, 5000):
+        G = torch.rand((n, n), dtype=torch.float32, device=dev) * 100.0
+        ms = _ms_per_sweep(lib, h, n, G)
+        gbs = n * n * 4 / (ms * 1e-3) / 1e9
+        out[f"sinkhorn_sweep_n{n}"] = {"us": ms * 1e3, "GB_s": gbs, "frac_hbm": gbs / hbm_peak,
+                                       "bytes": n * n * 4}
+        del G
+    for n, sym in ((2000, False), (5000, True)):
+        g = torch.Generator(device=dev).manual_seed(n)
+        A = (torch.rand((n, n), device=dev, generator=g) < 0.3).float()
+        B = (torch.rand((n, n), device=dev, generator=g) < 0.3).float()
+        if sym:
+            A = torch.triu(A, 1); A = A + A.T
+            B = torch.triu(B, 1); B = B + B.T
+        X = torch.rand((n, n), device=dev, generator=g)
+        X = X / X.sum(1, keepdim=True)
+        ms = ctypes.c_double(); prods = ctypes.c_int32(); terms = ctypes.c_int32()
+        _lib.check(lib.goat_bench_gradient(h.ptr, n, A.data_ptr(), B.data_ptr(), X.data_ptr(), 5,
+                                           ctypes.byref(ms), ctypes.byref(prods), ctypes.byref(terms)))
+        useful = prods.value * 2.0 * n ** 3 / (ms.value * 1e-3) / 1e12
+        issued = useful * max(1, terms.value)
+        out[f"gradient_n{n}_{'sym' if sym else 'directed'}"] = {
+            "ms": ms.value, "useful_TFLOP_s": useful, "issued_bf16_TFLOP_s": issued,
+            "frac_bf16_issued": issued / tf_peak, "bf16_terms_per_product": terms.value,
+            "peak": tf_peak, "peak_kind": tf_kind}
+        del A, B, X
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():

@@ -150,6 +150,14 @@ int goat_set_stream(goat_handle *h, void *stream);
 int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int32_t reps,
                      double *ms_per_sweep);
 
+/* Measurement hook (bench.py GEMM TFLOP/s): the gradient A X B^T + A^T X B on
+ * device matrices (handle precision, leading dim = n) `reps` times after one
+ * untimed preparation; *ms = mean time per gradient (CUDA events), *products =
+ * number of n^3 products it performed (2 symmetric, 4 directed), *terms = bf16
+ * split terms issued per product on the tcgen05 path (0 on the SIMT path). */
+int goat_bench_gradient(goat_handle *h, int64_t n, const void *dA, const void *dB, const void *dX,
+                        int32_t reps, double *ms, int32_t *products, int32_t *terms);
+
 /* Library build/feature string, e.g. "goat sm_100a tcgen05". */
 const char *goat_version(void);
 

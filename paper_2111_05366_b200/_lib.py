@@ -91,6 +91,9 @@ def _bind(lib):
         "goat_set_stream": (ctypes.c_int, [H, ctypes.c_void_p]),
         "goat_bench_sweep": (ctypes.c_int, [H, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                             ctypes.c_int32, _c_double_p]),
+        "goat_bench_gradient": (ctypes.c_int, [H, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_int32, _c_double_p, _c_i32_p,
+                                               _c_i32_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -103,7 +106,8 @@ def _bind(lib):
 EXPORTS = ("goat_create", "goat_destroy", "goat_last_error", "goat_version", "goat_reserve",
            "goat_fw_core", "goat_fw_core_device", "goat_gradient", "goat_lot",
            "goat_sinkhorn_knopp", "goat_line_search_coeffs", "goat_lap",
-           "goat_qap_objective_perm", "goat_set_stream", "goat_bench_sweep")
+           "goat_qap_objective_perm", "goat_set_stream", "goat_bench_sweep",
+           "goat_bench_gradient")
 
 
 def load():

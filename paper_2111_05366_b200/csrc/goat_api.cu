@@ -895,6 +895,47 @@ int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int3
     });
 }
 
+int goat_bench_gradient(goat_handle *h, int64_t n, const void *dA, const void *dB, const void *dX, int32_t reps,
+                        double *ms, int32_t *products, int32_t *terms) {
+    return guarded([&] {
+        require(h && dA && dB && dX && ms && reps >= 1, "bad argument");
+        check_order(n);
+        ensure_workspace(*h, n);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            Ctx c(*h, (int)n);
+            const size_t es = sizeof(T);
+            auto cp = [&](const void *src, T *dst) {
+                GOAT_CUDA(cudaMemcpy2DAsync(dst, c.ld * es, src, n * es, n * es, n, cudaMemcpyDeviceToDevice, c.s));
+            };
+            GOAT_CUDA(cudaMemsetAsync(h->A.p, 0, h->A.bytes, c.s));
+            GOAT_CUDA(cudaMemsetAsync(h->B.p, 0, h->B.bytes, c.s));
+            GOAT_CUDA(cudaMemsetAsync(h->P.p, 0, h->P.bytes, c.s));
+            cp(dA, h->A.as<T>());
+            cp(dB, h->B.as<T>());
+            cp(dX, h->P.as<T>());
+            c.sym = is_symmetric<T>(c, h->A.as<T>()) && is_symmetric<T>(c, h->B.as<T>());
+            setup_gemm<T>(c, h->A.as<T>(), h->B.as<T>());
+            gradient<T>(c, h->A.as<T>(), h->B.as<T>(), h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());  // warm
+            cudaEvent_t e0, e1;
+            GOAT_CUDA(cudaEventCreate(&e0));
+            GOAT_CUDA(cudaEventCreate(&e1));
+            GOAT_CUDA(cudaEventRecord(e0, c.s));
+            for (int r = 0; r < reps; ++r)
+                gradient<T>(c, h->A.as<T>(), h->B.as<T>(), h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());
+            GOAT_CUDA(cudaEventRecord(e1, c.s));
+            GOAT_CUDA(cudaEventSynchronize(e1));
+            float t = 0;
+            GOAT_CUDA(cudaEventElapsedTime(&t, e0, e1));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            *ms = t / reps;
+            if (products) *products = c.sym ? 2 : 4;
+            if (terms) *terms = c.tc ? std::max(h->tc_na, h->split) : 0;
+        });
+    });
+}
+
 int goat_lap(goat_handle *h, int64_t n, const double *M, int64_t ldm, int32_t sense, int64_t *assignment,
              double *objective, int32_t *certified) {
     return guarded([&] {
