@@ -28,8 +28,9 @@ constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_BYTES = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int TC_THREADS = 128;
-constexpr int TMEM_COLS = 256;
+constexpr int kEpiWarps = 8;
+constexpr int TC_THREADS = 64 + 32 * kEpiWarps;  // TMA, MMA, 8 epilogue warps
+constexpr int TMEM_COLS = 512;                    // two 256-column chunk accumulators
 constexpr size_t TC_SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -106,6 +107,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (+ TMEM owner),
+// warps 2..9 = promotion/epilogue.  The MMA accumulates `chunk` k-steps into one
+// of two 256-column TMEM buffers; epilogue warp w drains TMEM lane group w%4,
+// column half (w-2)/4, of each finished chunk into 128 fp32 registers with
+// round-to-nearest adds while the MMA fills the other buffer.  This bounds the
+// tensor core's truncating fp32 accumulation to `chunk` steps (promotion).
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -113,14 +124,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
     uint8_t *sB = smem + STAGES * A_BYTES;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
     uint64_t *empty = full + STAGES;
-    uint64_t *accum = empty + STAGES;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 1);
+    uint64_t *cfull = empty + STAGES;  // [2] MMA -> epilogue: chunk accumulated
+    uint64_t *cempty = cfull + 2;      // [2] epilogue -> MMA: chunk drained
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(cempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-        mbar_init(accum, 1);
+        for (int b = 0; b < 2; ++b) { mbar_init(cfull + b, 1); mbar_init(cempty + b, kEpiWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int t = 0; t < p.nterms; ++t) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.terms[t].a)) : "memory");
@@ -136,10 +148,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    // split-K slice of this CTA: steps [i0, i0 + total) of the flattened
-    // (term, k-block) sequence, so each accumulation chain stays short.
+    // split-K slice of this CTA: steps [i0, i0 + total) of the flattened (term, k-block) sequence
     const int i0 = blockIdx.z * p.kpb;
     const int total = max(0, min(p.nterms * p.kblocks, i0 + p.kpb) - i0);
+    const int C = max(1, p.chunk);
+    const int nchunks = (total + C - 1) / C;
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
@@ -157,57 +170,84 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
         if (lane == 0) {  // MMA issuer
             constexpr uint32_t idesc = idesc_bf16(BM, BN);
             for (int it = 0; it < total; ++it) {
+                const int c = it / C, b = c & 1;
+                const bool first = (it % C) == 0;
+                if (first && c >= 2) mbar_wait(cempty + b, ((c >> 1) - 1) & 1);
                 const int s = it % STAGES;
                 mbar_wait(full + s, (it / STAGES) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+                const uint32_t d = tmem + (uint32_t)(b * BN);
 #pragma unroll
                 for (int k = 0; k < BK / 16; ++k)  // 16 bf16 = 32 bytes along K inside the swizzle atom
-                    umma_bf16(tmem, sdesc(a0 + 32 * k), sdesc(b0 + 32 * k), idesc, (it | k) != 0);
+                    umma_bf16(d, sdesc(a0 + 32 * k), sdesc(b0 + 32 * k), idesc, (!first || k > 0) ? 1u : 0u);
                 umma_commit(empty + s);  // frees the stage once these MMAs have read it
+                if ((it % C) == C - 1 || it == total - 1) umma_commit(cfull + b);
             }
-            umma_commit(accum);
         }
         __syncwarp();
-    }
-
-    // Epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows m0 + 32w + lane.
-    if (total > 0) mbar_wait(accum, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int row = m0 + warp * 32 + lane;
-    const bool row_ok = row < p.M;
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, r);
-        const int col0 = n0 + c0;
-        if (!row_ok || col0 >= p.N) continue;
-        float v[16];
+    } else {
+        // Promotion + epilogue
+        const int lg = warp & 3, half = (warp - 2) >> 2;
+        float acc[128];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = total > 0 ? p.alpha * __uint_as_float(r[j]) : 0.f;
-        const bool full16 = col0 + 16 <= p.N;
-        if (p.mode == 0) {
-            float *dst = p.C + blockIdx.z * p.slice_stride + (int64_t)row * p.ldc + col0;
-            if (full16) {
+        for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+        const uint32_t tbase = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(half * 128);
+        for (int c = 0; c < nchunks; ++c) {
+            const int b = c & 1;
+            mbar_wait(cfull + b, (c >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-                for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else {
-                for (int j = 0; j < 16 && col0 + j < p.N; ++j) dst[j] = v[j];
+            for (int j = 0; j < 8; ++j) {
+                uint32_t r[16];
+                tmem_ld16(tbase + (uint32_t)(b * BN + j * 16), r);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) acc[j * 16 + q] += __uint_as_float(r[q]);
             }
-        } else {
-            // split fp32 -> bf16 planes: hi = rn(v), mid = rn(v - hi), lo = rn(v - hi - mid)
-            for (int pl = 0; pl < p.nplanes; ++pl) {
-                __nv_bfloat16 *dst = p.planes + pl * p.plane_stride + (int64_t)row * p.ldpl + col0;
-                __nv_bfloat16 b[16];
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(cempty + b);
+        }
+        const int row = m0 + lg * 32 + lane;
+        if (row < p.M) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    b[j] = __float2bfloat16_rn(v[j]);
-                    v[j] -= __bfloat162float(b[j]);
-                }
-                if (full16) {
-                    *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<uint4 *>(b);
-                    *reinterpret_cast<uint4 *>(dst + 8) = *reinterpret_cast<uint4 *>(b + 8);
+            for (int j = 0; j < 8; ++j) {
+                const int col0 = n0 + half * 128 + j * 16;
+                if (col0 >= p.N) continue;
+                float v[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = p.alpha * acc[j * 16 + q];
+                const bool full16 = col0 + 16 <= p.N;
+                if (p.mode == 0) {
+                    float *dst = p.C + blockIdx.z * p.slice_stride + (int64_t)row * p.ldc + col0;
+                    if (full16) {
+#pragma unroll
+                        for (int q = 0; q < 16; q += 4)
+                            *reinterpret_cast<float4 *>(dst + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+                    } else {
+                        for (int q = 0; q < 16 && col0 + q < p.N; ++q) dst[q] = v[q];
+                    }
                 } else {
-                    for (int j = 0; j < 16 && col0 + j < p.N; ++j) dst[j] = b[j];
+                    // split fp32 -> bf16 planes: hi = rn(v), mid = rn(v - hi), lo = rn(v - hi - mid)
+                    for (int pl = 0; pl < p.nplanes; ++pl) {
+                        __nv_bfloat16 *dst = p.planes + pl * p.plane_stride + (int64_t)row * p.ldpl + col0;
+                        uint32_t w[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const __nv_bfloat16 lo = __float2bfloat16_rn(v[2 * q]);
+                            const __nv_bfloat16 hi = __float2bfloat16_rn(v[2 * q + 1]);
+                            v[2 * q] -= __bfloat162float(lo);
+                            v[2 * q + 1] -= __bfloat162float(hi);
+                            w[q] = (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
+                        }
+                        if (full16) {
+                            *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+                            *reinterpret_cast<uint4 *>(dst + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+                        } else {
+                            for (int q = 0; q < 16 && col0 + q < p.N; ++q)
+                                dst[q] = __ushort_as_bfloat16((unsigned short)(w[q >> 1] >> (16 * (q & 1))));
+                        }
+                    }
                 }
             }
         }

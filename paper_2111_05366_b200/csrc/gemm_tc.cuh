@@ -26,6 +26,7 @@ struct TcGemmParams {
     int M, N, K, kblocks;
     int kslices;           // split-K: CTA z covers steps [z*kpb, (z+1)*kpb) of the
     int kpb;               //   flattened (term, k-block) sequence
+    int chunk;             // k-steps per TMEM chunk before promotion into fp32 registers
     int64_t slice_stride;  // elements between slice outputs (mode 0)
     float alpha;
     int mode;  // 0: fp32 C (slice z at C + z*slice_stride); 1: bf16 planes (kslices == 1 only)

@@ -168,17 +168,20 @@ void tc_gradient(Ctx &c, const float *X, float *out) {
     // Split-K: the tensor core's fp32 accumulation error grows with the number of
     // chained MMAs, so the K range is cut into slices reduced in fixed order with
     // round-to-nearest adds; slices also fill the SMs when there are few tiles.
-    // Steps per slice: <= 2 (term, k-block) steps when workspace allows (measured:
-    // error ~1e-6 of max|G| at n<=3000), at most 16 slices, <= 2 GiB of slices.
+    // Accuracy comes from in-kernel promotion (chunk k-steps per TMEM chain);
+    // split-K slices only fill the SMs when there are few output tiles.
     auto set_slices = [&](TcGemmParams &g, int rows) {
         const int steps = g.nterms * kblocks;
-        int sl = std::min(16, ceil_div(steps, 2));
+        const int tiles = ceil_div(n, tc_block_n()) * ceil_div(rows, tc_block_m());
+        int sl = std::min(8, ceil_div(2 * h.num_sms, tiles));
         if (const char *e = getenv("GOAT_TC_KSLICES")) sl = std::max(1, atoi(e));
         const int64_t cap = (int64_t)1 << 31;
         while (sl > 1 && (int64_t)sl * rows * ld * 4 > cap) --sl;
         sl = std::max(1, std::min(sl, steps));
         g.kpb = ceil_div(steps, sl);
         g.kslices = ceil_div(steps, g.kpb);
+        const char *ce = getenv("GOAT_TC_CHUNK");
+        g.chunk = ce ? std::max(1, atoi(ce)) : 4;  // measured: 2-6e-7 of max|G|, speed flat in chunk
     };
     static thread_local TcGemmParams g1, g2;
     // Y^T = [B; B^T] X^T
