@@ -315,11 +315,11 @@ def ctypes_ptr(x):
     return ctypes.c_void_p(int(x))
 
 
-def _ms_per_sweep(lib, h, n, G):
+def _ms_per_sweep(lib, h, n, G, reps=200):
     import ctypes
     from paper_2111_05366_b200 import _lib
     out = ctypes.c_double()
-    _lib.check(lib.goat_bench_sweep(h.ptr, n, G.data_ptr(), n, 200, ctypes.byref(out)))
+    _lib.check(lib.goat_bench_sweep(h.ptr, n, G.data_ptr(), n, reps, ctypes.byref(out)))
     return out.value
 
 
@@ -340,9 +340,9 @@ def _kernel_scan(lib, h, dev, hbm_peak):
     from paper_2111_05366_b200 import _lib
     out = {}
     tf_peak, tf_kind = _bf16_peak()
-    for n in (2000, 5000):
+    for n in (2000, 5000, 40000):
         G = torch.rand((n, n), dtype=torch.float32, device=dev) * 100.0
-        ms = _ms_per_sweep(lib, h, n, G)
+        ms = _ms_per_sweep(lib, h, n, G, reps=200 if n < 10000 else 20)
         gbs = n * n * 4 / (ms * 1e-3) / 1e9
         out[f"sinkhorn_sweep_n{n}"] = {"us": ms * 1e3, "GB_s": gbs, "frac_hbm": gbs / hbm_peak,
                                        "bytes": n * n * 4}

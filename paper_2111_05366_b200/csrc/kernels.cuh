@@ -21,6 +21,7 @@ struct SkArgs {
     SkState *st;
     int nblk;           // CTAs of the pass kernel
     unsigned long long *dslot = nullptr;  // persistent driver: atomicMax dev slots [row k&1 | col]
+    int slice_w = 0;    // cluster-split rows: columns per CTA rank
 };
 
 struct SkPlan {
@@ -29,6 +30,9 @@ struct SkPlan {
     int nblk = 0;      // pass-kernel CTAs
     int merge_blocks = 0;
     bool persistent = false;  // one cooperative launch for the whole sweep loop
+    int cl = 1;               // CTAs per row group (thread-block cluster) sharing each row
+    int ngrp = 0;             // row groups (= nblk / cl)
+    int slice_w = 0;          // columns per CTA rank when cl > 1
     size_t colpart_bytes = 0;
 };
 

@@ -80,15 +80,47 @@ __device__ __forceinline__ double *fslot(const SkArgs &a, int s) { return (s & 1
 __device__ __forceinline__ double *gslot(const SkArgs &a, int s) { return (s & 1) ? a.g[1] : a.g[0]; }
 
 // ------------------------------------------------------------------ pass body
-// Rows band-cyclic over CTAs (band = blk, blk + nblk, ...), so a CTA owns the
-// same rows every pass; columns are owned per thread (16-byte chunks).
-template <class T, int CH, int R>
+// Row bands are cyclic over row groups (grp, grp + ngrp, ...), so a group owns
+// the same rows every pass.  With CL == 1 a group is one CTA that owns whole
+// rows; with CL > 1 a group is a thread-block cluster whose CTA `rank` owns the
+// column slice [c0, c1): each CTA reduces its slice of every row, the per-row
+// (max, sum) pairs are exchanged through distributed shared memory (one cluster
+// barrier per band) and every CTA combines them in rank order, so all CTAs of the
+// cluster hold bit-identical row results.  Columns are owned per thread
+// (16-byte chunks of the slice).
+struct Slice {
+    int c0, c1;     // this CTA's columns
+    int grp, ngrp;  // row group (cluster) and number of groups
+    int rank;       // rank in the cluster (0 when CL == 1)
+};
+
+__device__ __forceinline__ uint32_t dsmem_map(const void *p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t addr, float) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_dsmem(uint32_t addr, double) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <class T, int CH, int R, int CL>
 __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
-                                          int blk, int nblk) {
+                                          const Slice &sl) {
     using V = typename VecT<T>::V;
     constexpr int VW = VecT<T>::W;
     constexpr int NW = kThreads / 32;
     __shared__ T s_m[2][NW][R], s_s[2][NW][R];
+    __shared__ T s_xm[2][R], s_xs[2][R];  // this CTA's per-row pair, read by cluster peers
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = a.n;
     const bool pre = (k == 0);
@@ -100,16 +132,8 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
     const double ks = SkMath<T>::kScale;
     const T coef = (T)(coef_d * ks);
     const T gmax = (T)gmax_d;
-
-    T gl[CH][VW], acc[CH][VW];
-#pragma unroll
-    for (int c = 0; c < CH; ++c)
-#pragma unroll
-        for (int e = 0; e < VW; ++e) {
-            const int col = (tid + kThreads * c) * VW + e;
-            gl[c][e] = (col < n && !pre) ? (T)(__ldcg(gin + col) * ks) : T(0);
-            acc[c][e] = T(0);
-        }
+    const int c0 = sl.c0, c1 = sl.c1;
+    const bool writer = (sl.rank == 0);  // one CTA per group writes f / deviation
 
     double devmax = 0.0;
     const int nbands = (n + R - 1) / R;
@@ -121,16 +145,27 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         for (int r = 0; r < R; ++r)
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
-                const int q = tid + kThreads * c;
+                const int col = c0 + (tid + kThreads * c) * VW;
                 const int row = band * R + r;
-                if (band < nbands && row < n && q * VW < n)
-                    dst[r][c] = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + (int64_t)q * VW));
+                if (band < nbands && row < n && col < c1)
+                    dst[r][c] = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + col));
                 else
                     memset(&dst[r][c], 0, sizeof(V));
             }
     };
-    load_band(blk, xv);
-    for (int band = blk; band < nbands; band += nblk) {
+    load_band(sl.grp, xv);
+
+    T gl[CH][VW], acc[CH][VW];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+            const int col = c0 + (tid + kThreads * c) * VW + e;
+            gl[c][e] = (col < c1 && !pre) ? (T)(__ldcg(gin + col) * ks) : T(0);
+            acc[c][e] = T(0);
+        }
+
+    for (int band = sl.grp; band < nbands; band += sl.ngrp) {
         const int r0 = band * R;
         T x[R][CH][VW];
 #pragma unroll
@@ -141,10 +176,10 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
 #pragma unroll
                 for (int e = 0; e < VW; ++e) x[r][c][e] = pv[e];
             }
-        load_band(band + nblk, xv);  // prefetch
+        load_band(band + sl.ngrp, xv);  // prefetch
         // f_{k-1} of row r0 + lane (warp 0 checks the deviation), fetched early
         double fprev_v = 0.0;
-        if (warp == 0 && lane < R && k >= 2 && r0 + lane < n) fprev_v = __ldcg(fprev + r0 + lane);
+        if (writer && warp == 0 && lane < R && k >= 2 && r0 + lane < n) fprev_v = __ldcg(fprev + r0 + lane);
         T m[R], s[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -154,9 +189,9 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
             for (int c = 0; c < CH; ++c)
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
-                    const int col = (tid + kThreads * c) * VW + e;
+                    const int col = c0 + (tid + kThreads * c) * VW + e;
                     // E_ij = coef * (gmax - G_ij), reference order (sinkhorn.py:125)
-                    const T arg = (rv && col < n) ? coef * (gmax - x[r][c][e]) + gl[c][e] : neg_inf<T>();
+                    const T arg = (rv && col < c1) ? coef * (gmax - x[r][c][e]) + gl[c][e] : neg_inf<T>();
                     x[r][c][e] = arg;
                     m[r] = arg > m[r] ? arg : m[r];
                 }
@@ -191,26 +226,47 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         // Per-warp pairs into a parity-double-buffered slot: one block barrier per
         // band; every warp then finishes all R rows itself (lane r <- row r) in
         // the same fixed order, so the results agree bit-for-bit across warps.
-        const int par = ((band - blk) / nblk) & 1;
+        const int par = ((band - sl.grp) / sl.ngrp) & 1;
         if (lane == 0) {
 #pragma unroll
             for (int r = 0; r < R; ++r) { s_m[par][warp][r] = m[r]; s_s[par][warp][r] = s[r]; }
         }
         __syncthreads();
-        double lse_l = 0.0;
+        T Mb = neg_inf<T>(), Sb = T(0);
         if (lane < R) {
-            T M = neg_inf<T>();
 #pragma unroll
-            for (int w = 0; w < NW; ++w) { const T mw = s_m[par][w][lane]; M = mw > M ? mw : M; }
-            T S = T(0);
+            for (int w = 0; w < NW; ++w) { const T mw = s_m[par][w][lane]; Mb = mw > Mb ? mw : Mb; }
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
                 const T mw = s_m[par][w][lane];
-                if (mw != neg_inf<T>()) S += s_s[par][w][lane] * SkMath<T>::ex(mw - M);
+                if (mw != neg_inf<T>()) Sb += s_s[par][w][lane] * SkMath<T>::ex(mw - Mb);
             }
-            lse_l = (double)M + SkMath<T>::lgt(S);  // scaled units
+        }
+        if constexpr (CL > 1) {
+            // cluster combine: publish this CTA's pair, meet, combine all ranks in order
+            if (warp == 0 && lane < R) { s_xm[par][lane] = Mb; s_xs[par][lane] = Sb; }
+            cluster_sync();
+            if (lane < R) {
+                T mq[CL], sq[CL];
+#pragma unroll
+                for (int q = 0; q < CL; ++q) {
+                    mq[q] = ld_dsmem(dsmem_map(&s_xm[par][lane], q), T(0));
+                    sq[q] = ld_dsmem(dsmem_map(&s_xs[par][lane], q), T(0));
+                }
+                Mb = neg_inf<T>();
+#pragma unroll
+                for (int q = 0; q < CL; ++q) Mb = mq[q] > Mb ? mq[q] : Mb;
+                Sb = T(0);
+#pragma unroll
+                for (int q = 0; q < CL; ++q)
+                    if (mq[q] != neg_inf<T>()) Sb += sq[q] * SkMath<T>::ex(mq[q] - Mb);
+            }
+        }
+        double lse_l = 0.0;
+        if (lane < R) {
+            lse_l = (double)Mb + SkMath<T>::lgt(Sb);  // scaled units
             const int row = r0 + lane;
-            if (warp == 0 && row < n) {
+            if (writer && warp == 0 && row < n) {
                 const double fnew = -lse_l / ks;
                 double dev = 0.0;
                 if (pre) dev = SkMath<T>::dev(-fnew);                  // |rowsum(K) - 1|
@@ -236,17 +292,21 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
             }
         }
     }
+    if constexpr (CL > 1) {
+        // keep peers' DSMEM slots alive until every CTA of the cluster is done
+        cluster_sync();
+    }
     if (!rowonly) {
-        T *cp = static_cast<T *>(a.colpart) + (int64_t)blk * a.ldp;
+        T *cp = static_cast<T *>(a.colpart) + (int64_t)sl.grp * a.ldp;
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
-            const int q = tid + kThreads * c;
-            if (q * VW < n) {
+            const int col = c0 + (tid + kThreads * c) * VW;
+            if (col < c1) {
                 V v;
                 T *pv = reinterpret_cast<T *>(&v);
 #pragma unroll
                 for (int e = 0; e < VW; ++e) pv[e] = acc[c][e];
-                __stcg(reinterpret_cast<V *>(cp + (int64_t)q * VW), v);
+                __stcg(reinterpret_cast<V *>(cp + col), v);
             }
         }
     }
@@ -259,7 +319,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
     if (tid == 0) {
         double d = 0.0;
         for (int w = 0; w < NW; ++w) d = fmax(d, s_dev[w]);
-        __stcg(a.devpart + blk, d);
+        __stcg(a.devpart + blockIdx.x, d);
         // max of non-negative doubles == max of their bit patterns: order-independent
         if (a.dslot) atomicMax(a.dslot + (k & 1), (unsigned long long)__double_as_longlong(d));
     }
@@ -378,7 +438,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks, un
 }
 
 // ------------------------------------------------------------------ drivers
-template <class T, int CH, int R>
+template <class T, int CH, int R, int CL>
 __global__ void __launch_bounds__(kThreads, 2) sk_persistent_kernel(SkArgs a, unsigned *bar) {
     __shared__ int s_k;
     if (threadIdx.x == 0) s_k = a.st->k;
@@ -387,9 +447,21 @@ __global__ void __launch_bounds__(kThreads, 2) sk_persistent_kernel(SkArgs a, un
     const int K = a.st->max_sweeps;
     const double tol = a.st->tol, coef = a.st->coef, gmax = a.st->gmax;
     const int blk = blockIdx.x, nblk = gridDim.x;
+    Slice sl{0, a.n, blk, nblk, 0};
+    if constexpr (CL > 1) {
+        uint32_t rank, cid, ncl;
+        asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+        asm("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
+        sl.rank = (int)rank;
+        sl.grp = (int)cid;
+        sl.ngrp = (int)ncl;
+        sl.c0 = min(a.n, (int)rank * a.slice_w);
+        sl.c1 = min(a.n, sl.c0 + a.slice_w);
+    }
     unsigned epoch = 0;
     for (int k = k0;; ++k) {
-        pass_body<T, CH, R>(a, k, K, coef, gmax, blk, nblk);
+        pass_body<T, CH, R, CL>(a, k, K, coef, gmax, sl);
         grid_barrier(bar, nblk, epoch);
         const double drow = __longlong_as_double((long long)__ldcg(a.dslot + (k & 1)));
         if (blk == 0 && threadIdx.x == 0) a.dslot[(k + 1) & 1] = 0ull;  // next sweep's slot
@@ -429,7 +501,8 @@ __global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
     }
     __syncthreads();
     if (s_done) return;
-    pass_body<T, CH, R>(a, s_k, a.st->max_sweeps, a.st->coef, a.st->gmax, blockIdx.x, gridDim.x);
+    const Slice sl{0, a.n, (int)blockIdx.x, (int)gridDim.x, 0};
+    pass_body<T, CH, R, 1>(a, s_k, a.st->max_sweeps, a.st->coef, a.st->gmax, sl);
 }
 
 template <class T>
@@ -533,20 +606,56 @@ __global__ void __launch_bounds__(kThreads) sk_emit_kernel(SkArgs a, T *Q, int64
 constexpr int kMaxCh = 8;
 constexpr int rows_for(int ch) { return ch == 1 ? 8 : ch == 2 ? 4 : ch <= 4 ? 2 : 1; }
 
-template <class T, int CH> void *persistent_fn() { return (void *)sk_persistent_kernel<T, CH, rows_for(CH)>; }
+template <class T, int CH, int CL> void *persistent_fn() {
+    return (void *)sk_persistent_kernel<T, CH, rows_for(CH), CL>;
+}
 
-template <class T> void *persistent_for(int ch) {
-    switch (ch) {
-        case 1: return persistent_fn<T, 1>();
-        case 2: return persistent_fn<T, 2>();
-        case 3: return persistent_fn<T, 3>();
-        case 4: return persistent_fn<T, 4>();
-        case 5: return persistent_fn<T, 5>();
-        case 6: return persistent_fn<T, 6>();
-        case 7: return persistent_fn<T, 7>();
-        case 8: return persistent_fn<T, 8>();
+// CL == 1 for any CH; clusters only when one CTA cannot hold a row (CH of the slice >= 4).
+template <class T> void *persistent_for(int ch, int cl) {
+    if (cl == 1) {
+        switch (ch) {
+            case 1: return persistent_fn<T, 1, 1>();
+            case 2: return persistent_fn<T, 2, 1>();
+            case 3: return persistent_fn<T, 3, 1>();
+            case 4: return persistent_fn<T, 4, 1>();
+            case 5: return persistent_fn<T, 5, 1>();
+            case 6: return persistent_fn<T, 6, 1>();
+            case 7: return persistent_fn<T, 7, 1>();
+            case 8: return persistent_fn<T, 8, 1>();
+        }
     }
-    throw Error(GOAT_ENOTSUP, "sinkhorn: bad chunk count");
+#define GOAT_CL(C)                                         \
+    if (cl == C) {                                         \
+        switch (ch) {                                      \
+            case 4: return persistent_fn<T, 4, C>();       \
+            case 5: return persistent_fn<T, 5, C>();       \
+            case 6: return persistent_fn<T, 6, C>();       \
+            case 7: return persistent_fn<T, 7, C>();       \
+            case 8: return persistent_fn<T, 8, C>();       \
+        }                                                  \
+    }
+    GOAT_CL(2)
+    GOAT_CL(4)
+    GOAT_CL(8)
+#undef GOAT_CL
+    throw Error(GOAT_ENOTSUP, "sinkhorn: no kernel for chunks=" + std::to_string(ch) + " cluster=" + std::to_string(cl));
+}
+
+cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunchAttribute (&attrs)[2]) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.nblk);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    attrs[0].id = cudaLaunchAttributeCooperative;
+    attrs[0].val.cooperative = 1;
+    attrs[1].id = cudaLaunchAttributeClusterDimension;
+    attrs[1].val.clusterDim.x = p.cl;
+    attrs[1].val.clusterDim.y = 1;
+    attrs[1].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = p.cl > 1 ? 2 : 1;
+    return cfg;
 }
 
 int env_int(const char *name, int dflt) {
@@ -559,25 +668,45 @@ int env_int(const char *name, int dflt) {
 template <class T> SkPlan sk_plan(int n, int num_sms) {
     constexpr int VW = VecT<T>::W;
     SkPlan p;
-    const int chunks = (n + VW - 1) / VW;
-    p.ch = (chunks + kThreads - 1) / kThreads;
+    // Row width per CTA: whole rows when they fit kMaxCh chunks per thread,
+    // else a cluster of cl CTAs splits each row into column slices.
+    p.cl = 1;
+    p.slice_w = (int)round_up(n, 8 * VW);
+    p.ch = ceil_div(ceil_div(n, VW), kThreads);
+    while (p.ch > kMaxCh && p.cl < 8) {
+        p.cl *= 2;
+        p.slice_w = (int)round_up(ceil_div(n, p.cl), 8 * VW);
+        p.ch = std::max(4, ceil_div(ceil_div(p.slice_w, VW), kThreads));
+    }
     if (p.ch > kMaxCh)
-        throw Error(GOAT_ENOTSUP, "sinkhorn: order " + std::to_string(n) +
-                                      " exceeds the single-CTA row width of this build");
+        throw Error(GOAT_ENOTSUP, "sinkhorn: order " + std::to_string(n) + " exceeds 8-CTA clusters of this build");
     p.rows = rows_for(p.ch);
     const int nbands = (n + p.rows - 1) / p.rows;
-    // Persistent (cooperative) driver: every CTA must be co-resident.  Fewer CTAs
-    // make the two grid barriers per sweep cheaper; aim for >= ~64 KB of G per CTA.
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)persistent_for<T>(p.ch), kThreads, 0);
-    const int coresident = std::max(1, occ) * num_sms;
-    // Measured (profiles/round1_sk_tune.json): per-sweep time falls monotonically
-    // with CTA count up to one CTA per SM at every n tested (1000..5000).
-    const int want = coresident;
-    p.persistent = env_int("GOAT_SK_PERSISTENT", 1) != 0 && occ > 0;
-    p.nblk = std::max(1, std::min({nbands, coresident, want}));
-    if (const int force = env_int("GOAT_SK_BLOCKS", 0)) p.nblk = std::max(1, std::min({force, nbands, coresident}));
-    if (!p.persistent) p.nblk = std::max(1, std::min(nbands, num_sms));
+    p.persistent = env_int("GOAT_SK_PERSISTENT", 1) != 0 || p.cl > 1;
+    // Co-resident groups (CTAs, or clusters of cl CTAs) for the cooperative launch.
+    int groups = 0;
+    if (p.cl == 1) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)persistent_for<T>(p.ch, 1), kThreads, 0);
+        groups = std::max(1, occ) * num_sms;  // measured: all co-resident CTAs is fastest (n <= 5000)
+    } else {
+        cudaLaunchAttribute attrs[2];
+        SkPlan q = p;
+        q.nblk = p.cl * num_sms;
+        cudaLaunchConfig_t cfg = persistent_config(q, nullptr, attrs);
+        cfg.numAttrs = 0;  // occupancy query takes the cluster shape, not the cooperative flag
+        cudaLaunchAttribute cattr = attrs[1];
+        cfg.attrs = &cattr;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        GOAT_CUDA(cudaOccupancyMaxActiveClusters(&ncl, persistent_for<T>(p.ch, p.cl), &cfg));
+        groups = std::max(1, ncl);
+    }
+    int ngrp = std::max(1, std::min(nbands, groups));
+    if (const int force = env_int("GOAT_SK_BLOCKS", 0)) ngrp = std::max(1, std::min({force / p.cl, nbands, groups}));
+    if (!p.persistent) ngrp = std::max(1, std::min(nbands, num_sms));
+    p.ngrp = ngrp;
+    p.nblk = ngrp * p.cl;
     p.merge_blocks = std::max(1, std::min((n + 7) / 8, 4 * num_sms));  // one warp per column
     p.colpart_bytes = (size_t)std::max(p.nblk, num_sms * 2) * round_up(n, 8) * sizeof(T);
     return p;
@@ -590,6 +719,7 @@ void launch_pass_ch(const SkArgs &a, const SkPlan &p, cudaStream_t s) {
 }
 
 template <class T> void sk_launch_pass(const SkArgs &a, const SkPlan &p, cudaStream_t s) {
+    if (p.cl != 1) throw Error(GOAT_ENOTSUP, "sinkhorn: cluster-split rows need the persistent driver");
     switch (p.ch) {
         case 1: launch_pass_ch<T, 1>(a, p, s); break;
         case 2: launch_pass_ch<T, 2>(a, p, s); break;
@@ -614,8 +744,12 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
     GOAT_CUDA(cudaMemsetAsync(bar, 0, 1024, s));
     SkArgs args = a;
     args.dslot = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(bar) + 512);
+    args.nblk = p.ngrp;  // column-partial rows = row groups
+    args.slice_w = p.slice_w;
     void *params[] = {&args, &bar};
-    GOAT_CUDA(cudaLaunchCooperativeKernel(persistent_for<T>(p.ch), dim3(p.nblk), dim3(kThreads), params, 0, s));
+    cudaLaunchAttribute attrs[2];
+    cudaLaunchConfig_t cfg = persistent_config(p, s, attrs);
+    GOAT_CUDA(cudaLaunchKernelExC(&cfg, persistent_for<T>(p.ch, p.cl), params));
     note_launch();
 }
 
