@@ -109,18 +109,55 @@ __device__ __forceinline__ double ld_dsmem(uint32_t addr, double) {
     asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
     return v;
 }
+// Remote (DSMEM) store of a pair that signals the receiver's mbarrier on arrival.
+__device__ __forceinline__ void st_async_pair(uint32_t raddr, float a, float b, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "f"(a), "f"(b), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_pair(uint32_t raddr, double a, double b, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "d"(a), "d"(b), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void xbar_init(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+}
+__device__ __forceinline__ void xbar_arm(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void xbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "XW_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra XW_%=;\n"
+        "}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Per-CTA exchange area for cluster-split rows: slot [parity][rank][row] holds a
+// (max, sum) pair written by peer `rank` with st.async; xbar[parity] counts the bytes.
+template <class T, int R, int CL> struct __align__(16) RowXch {
+    T pair[2][CL][R][2];
+    uint64_t bar[2];
+};
+
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 template <class T, int CH, int R, int CL>
 __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
-                                          const Slice &sl) {
+                                          const Slice &sl, RowXch<T, R, CL> *xch, unsigned &xi) {
     using V = typename VecT<T>::V;
     constexpr int VW = VecT<T>::W;
     constexpr int NW = kThreads / 32;
     __shared__ T s_m[2][NW][R], s_s[2][NW][R];
-    __shared__ T s_xm[2][R], s_xs[2][R];  // this CTA's per-row pair, read by cluster peers
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = a.n;
     const bool pre = (k == 0);
@@ -161,7 +198,11 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
 #pragma unroll
         for (int e = 0; e < VW; ++e) {
             const int col = c0 + (tid + kThreads * c) * VW + e;
-            gl[c][e] = (col < c1 && !pre) ? (T)(__ldcg(gin + col) * ks) : T(0);
+            // Column offset g_j; columns outside the slice get -inf, so masking costs
+            // nothing per element.  (E is formed as coef*(gmax - G) as in the
+            // reference; folding coef*gmax into g cancels catastrophically.)
+            const T gv = (!pre && col < c1) ? (T)(__ldcg(gin + col) * ks) : T(0);
+            gl[c][e] = col < c1 ? gv : neg_inf<T>();
             acc[c][e] = T(0);
         }
 
@@ -183,28 +224,31 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         T m[R], s[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const bool rv = (r0 + r) < n;
             m[r] = neg_inf<T>();
 #pragma unroll
             for (int c = 0; c < CH; ++c)
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
-                    const int col = c0 + (tid + kThreads * c) * VW + e;
-                    // E_ij = coef * (gmax - G_ij), reference order (sinkhorn.py:125)
-                    const T arg = (rv && col < c1) ? coef * (gmax - x[r][c][e]) + gl[c][e] : neg_inf<T>();
+                    const T arg = coef * (gmax - x[r][c][e]) + gl[c][e];  // E_ij + g_j (sinkhorn.py:125)
                     x[r][c][e] = arg;
                     m[r] = arg > m[r] ? arg : m[r];
                 }
         }
         // Warp max first (shuffle + max only), then exponentials against the warp
-        // max and a plain sum butterfly: no SFU op on the shuffle chain.
+        // max and a plain sum butterfly: no SFU op on the shuffle chain.  Rows past
+        // the end get m = -inf (skipped everywhere); exponentials use mx, which is
+        // 0 for an all-masked warp so exp(-inf - mx) = 0 (no NaN).
+        T mx[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+        for (int r = 0; r < R; ++r) {
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
                 const T m2 = __shfl_xor_sync(0xffffffffu, m[r], off);
                 m[r] = m2 > m[r] ? m2 : m[r];
             }
+            if (r0 + r >= n) m[r] = neg_inf<T>();
+            mx[r] = (m[r] == neg_inf<T>()) ? T(0) : m[r];
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             s[r] = T(0);
@@ -212,11 +256,11 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
             for (int c = 0; c < CH; ++c)
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
-                    const T arg = x[r][c][e];
-                    const T y = (arg == neg_inf<T>()) ? T(0) : SkMath<T>::ex(arg - m[r]);
+                    const T y = SkMath<T>::ex(x[r][c][e] - mx[r]);
                     x[r][c][e] = y;
                     s[r] += y;
                 }
+            if (m[r] == neg_inf<T>()) s[r] = T(0);
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -243,15 +287,27 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
             }
         }
         if constexpr (CL > 1) {
-            // cluster combine: publish this CTA's pair, meet, combine all ranks in order
-            if (warp == 0 && lane < R) { s_xm[par][lane] = Mb; s_xs[par][lane] = Sb; }
-            cluster_sync();
+            // cluster combine without a cluster barrier: warp 0 pushes this CTA's
+            // pairs into every peer's slot with st.async (mbarrier complete_tx);
+            // each warp waits for the CL-1 remote pairs and combines all ranks in
+            // rank order (its own pair from registers), identically in every CTA.
+            const int xp = xi & 1;
+            const uint32_t xph = (xi >> 1) & 1;
+            if (warp == 0 && lane == 0) xbar_arm(&xch->bar[xp], (uint32_t)((CL - 1) * R * 2 * sizeof(T)));
+            if (warp == 0 && lane < R) {
+#pragma unroll
+                for (int q = 0; q < CL; ++q)
+                    if (q != sl.rank)
+                        st_async_pair(dsmem_map(&xch->pair[xp][sl.rank][lane][0], q), Mb, Sb,
+                                      dsmem_map(&xch->bar[xp], q));
+            }
             if (lane < R) {
+                xbar_wait(&xch->bar[xp], xph);
                 T mq[CL], sq[CL];
 #pragma unroll
                 for (int q = 0; q < CL; ++q) {
-                    mq[q] = ld_dsmem(dsmem_map(&s_xm[par][lane], q), T(0));
-                    sq[q] = ld_dsmem(dsmem_map(&s_xs[par][lane], q), T(0));
+                    mq[q] = (q == sl.rank) ? Mb : xch->pair[xp][q][lane][0];
+                    sq[q] = (q == sl.rank) ? Sb : xch->pair[xp][q][lane][1];
                 }
                 Mb = neg_inf<T>();
 #pragma unroll
@@ -261,6 +317,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
                 for (int q = 0; q < CL; ++q)
                     if (mq[q] != neg_inf<T>()) Sb += sq[q] * SkMath<T>::ex(mq[q] - Mb);
             }
+            ++xi;
         }
         double lse_l = 0.0;
         if (lane < R) {
@@ -284,17 +341,13 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
                 if (m[r] == neg_inf<T>()) continue;
                 // column contribution y = x * exp(m + f_col), f_col = 0 on the pre-check
                 const double colf = pre ? 0.0 : -lse_r[r];
-                const T sc = SkMath<T>::ex((T)((double)m[r] + colf));
+                const T sc = SkMath<T>::ex((T)((double)mx[r] + colf));
 #pragma unroll
                 for (int c = 0; c < CH; ++c)
 #pragma unroll
                     for (int e = 0; e < VW; ++e) acc[c][e] += x[r][c][e] * sc;
             }
         }
-    }
-    if constexpr (CL > 1) {
-        // keep peers' DSMEM slots alive until every CTA of the cluster is done
-        cluster_sync();
     }
     if (!rowonly) {
         T *cp = static_cast<T *>(a.colpart) + (int64_t)sl.grp * a.ldp;
@@ -439,7 +492,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks, un
 
 // ------------------------------------------------------------------ drivers
 template <class T, int CH, int R, int CL>
-__global__ void __launch_bounds__(kThreads, 2) sk_persistent_kernel(SkArgs a, unsigned *bar) {
+__global__ void __launch_bounds__(kThreads, (CL > 1 ? 1 : 2)) sk_persistent_kernel(SkArgs a, unsigned *bar) {
     __shared__ int s_k;
     if (threadIdx.x == 0) s_k = a.st->k;
     __syncthreads();
@@ -459,9 +512,19 @@ __global__ void __launch_bounds__(kThreads, 2) sk_persistent_kernel(SkArgs a, un
         sl.c0 = min(a.n, (int)rank * a.slice_w);
         sl.c1 = min(a.n, sl.c0 + a.slice_w);
     }
+    __shared__ RowXch<T, R, CL> xch;
+    unsigned xi = 0;  // exchange counter (bands processed by this cluster so far)
+    if constexpr (CL > 1) {
+        if (threadIdx.x == 0) {
+            xbar_init(&xch.bar[0]);
+            xbar_init(&xch.bar[1]);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        cluster_sync();  // every peer's barriers exist before the first st.async
+    }
     unsigned epoch = 0;
     for (int k = k0;; ++k) {
-        pass_body<T, CH, R, CL>(a, k, K, coef, gmax, sl);
+        pass_body<T, CH, R, CL>(a, k, K, coef, gmax, sl, &xch, xi);
         grid_barrier(bar, nblk, epoch);
         const double drow = __longlong_as_double((long long)__ldcg(a.dslot + (k & 1)));
         if (blk == 0 && threadIdx.x == 0) a.dslot[(k + 1) & 1] = 0ull;  // next sweep's slot
@@ -487,6 +550,7 @@ __global__ void __launch_bounds__(kThreads, 2) sk_persistent_kernel(SkArgs a, un
                 a.st->done = 1; a.st->sweeps = sweeps; a.st->converged = conv; a.st->slot = slot;
                 a.st->k = k + 1;
             }
+            if constexpr (CL > 1) cluster_sync();
             return;
         }
     }
@@ -502,7 +566,8 @@ __global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
     __syncthreads();
     if (s_done) return;
     const Slice sl{0, a.n, (int)blockIdx.x, (int)gridDim.x, 0};
-    pass_body<T, CH, R, 1>(a, s_k, a.st->max_sweeps, a.st->coef, a.st->gmax, sl);
+    unsigned xi = 0;
+    pass_body<T, CH, R, 1>(a, s_k, a.st->max_sweeps, a.st->coef, a.st->gmax, sl, nullptr, xi);
 }
 
 template <class T>
@@ -605,9 +670,12 @@ __global__ void __launch_bounds__(kThreads) sk_emit_kernel(SkArgs a, T *Q, int64
 
 constexpr int kMaxCh = 8;
 constexpr int rows_for(int ch) { return ch == 1 ? 8 : ch == 2 ? 4 : ch <= 4 ? 2 : 1; }
+// Clustered (wide-row) kernels run one CTA per SM with more rows per band so the
+// per-band cluster barrier and reduction chain amortise over more bytes.
+constexpr int rows_for(int ch, int cl) { return cl == 1 ? rows_for(ch) : (ch <= 6 ? 4 : 2); }
 
 template <class T, int CH, int CL> void *persistent_fn() {
-    return (void *)sk_persistent_kernel<T, CH, rows_for(CH), CL>;
+    return (void *)sk_persistent_kernel<T, CH, rows_for(CH, CL), CL>;
 }
 
 // CL == 1 for any CH; clusters only when one CTA cannot hold a row (CH of the slice >= 4).
@@ -641,6 +709,11 @@ template <class T> void *persistent_for(int ch, int cl) {
     throw Error(GOAT_ENOTSUP, "sinkhorn: no kernel for chunks=" + std::to_string(ch) + " cluster=" + std::to_string(cl));
 }
 
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
 cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunchAttribute (&attrs)[2]) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.nblk);
@@ -648,7 +721,9 @@ cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunch
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     attrs[0].id = cudaLaunchAttributeCooperative;
-    attrs[0].val.cooperative = 1;
+    // GOAT_SK_NOCOOP=1 drops the cooperative flag (profilers cannot replay it);
+    // the grid is still sized to the co-resident maximum.
+    attrs[0].val.cooperative = env_int("GOAT_SK_NOCOOP", 0) ? 0 : 1;
     attrs[1].id = cudaLaunchAttributeClusterDimension;
     attrs[1].val.clusterDim.x = p.cl;
     attrs[1].val.clusterDim.y = 1;
@@ -658,10 +733,6 @@ cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunch
     return cfg;
 }
 
-int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
 
 }  // namespace
 
@@ -680,7 +751,7 @@ template <class T> SkPlan sk_plan(int n, int num_sms) {
     }
     if (p.ch > kMaxCh)
         throw Error(GOAT_ENOTSUP, "sinkhorn: order " + std::to_string(n) + " exceeds 8-CTA clusters of this build");
-    p.rows = rows_for(p.ch);
+    p.rows = rows_for(p.ch, p.cl);
     const int nbands = (n + p.rows - 1) / p.rows;
     p.persistent = env_int("GOAT_SK_PERSISTENT", 1) != 0 || p.cl > 1;
     // Co-resident groups (CTAs, or clusters of cl CTAs) for the cooperative launch.
