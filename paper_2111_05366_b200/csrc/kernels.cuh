@@ -31,6 +31,7 @@ struct SkPlan {
     int merge_blocks = 0;
     bool persistent = false;  // one cooperative launch for the whole sweep loop
     int cl = 1;               // CTAs per row group (thread-block cluster) sharing each row
+    int nt = 256;             // threads per CTA
     int ngrp = 0;             // row groups (= nblk / cl)
     int slice_w = 0;          // columns per CTA rank when cl > 1
     size_t colpart_bytes = 0;

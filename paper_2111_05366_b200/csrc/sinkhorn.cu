@@ -143,20 +143,20 @@ __device__ __forceinline__ void xbar_wait(uint64_t *bar, uint32_t parity) {
 // Per-CTA exchange area for cluster-split rows: slot [parity][rank][row] holds a
 // (max, sum) pair written by peer `rank` with st.async; xbar[parity] counts the bytes.
 template <class T, int R, int CL> struct __align__(16) RowXch {
-    T pair[2][CL][R][2];
-    uint64_t bar[2];
+    T pair[4][CL][R][2];
+    uint64_t bar[4];
 };
 
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <class T, int CH, int R, int CL>
+template <class T, int CH, int R, int CL, int NT>
 __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
                                           const Slice &sl, RowXch<T, R, CL> *xch, unsigned &xi) {
     using V = typename VecT<T>::V;
     constexpr int VW = VecT<T>::W;
-    constexpr int NW = kThreads / 32;
+    constexpr int NW = NT / 32;
     __shared__ T s_m[2][NW][R], s_s[2][NW][R];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = a.n;
@@ -182,7 +182,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         for (int r = 0; r < R; ++r)
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
-                const int col = c0 + (tid + kThreads * c) * VW;
+                const int col = c0 + (tid + NT * c) * VW;
                 const int row = band * R + r;
                 if (band < nbands && row < n && col < c1)
                     dst[r][c] = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + col));
@@ -197,7 +197,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
     for (int c = 0; c < CH; ++c)
 #pragma unroll
         for (int e = 0; e < VW; ++e) {
-            const int col = c0 + (tid + kThreads * c) * VW + e;
+            const int col = c0 + (tid + NT * c) * VW + e;
             // Column offset g_j; columns outside the slice get -inf, so masking costs
             // nothing per element.  (E is formed as coef*(gmax - G) as in the
             // reference; folding coef*gmax into g cancels catastrophically.)
@@ -291,8 +291,8 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
             // pairs into every peer's slot with st.async (mbarrier complete_tx);
             // each warp waits for the CL-1 remote pairs and combines all ranks in
             // rank order (its own pair from registers), identically in every CTA.
-            const int xp = xi & 1;
-            const uint32_t xph = (xi >> 1) & 1;
+            const int xp = xi & 3;
+            const uint32_t xph = (xi >> 2) & 1;
             if (warp == 0 && lane == 0) xbar_arm(&xch->bar[xp], (uint32_t)((CL - 1) * R * 2 * sizeof(T)));
             if (warp == 0 && lane < R) {
 #pragma unroll
@@ -353,7 +353,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         T *cp = static_cast<T *>(a.colpart) + (int64_t)sl.grp * a.ldp;
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
-            const int col = c0 + (tid + kThreads * c) * VW;
+            const int col = c0 + (tid + NT * c) * VW;
             if (col < c1) {
                 V v;
                 T *pv = reinterpret_cast<T *>(&v);
@@ -374,6 +374,203 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         for (int w = 0; w < NW; ++w) d = fmax(d, s_dev[w]);
         __stcg(a.devpart + blockIdx.x, d);
         // max of non-negative doubles == max of their bit patterns: order-independent
+        if (a.dslot) atomicMax(a.dslot + (k & 1), (unsigned long long)__double_as_longlong(d));
+    }
+}
+
+// Clustered wide rows (CL > 1, one row per band): the cross-CTA row exchange is
+// software-pipelined.  Iteration j reduces band j over this CTA's column slice and
+// pushes the (max, sum) pair to every peer (st.async + mbarrier), then finishes band
+// j-1 -- whose peer pairs have had a whole band to arrive -- with the row LSE, f,
+// the deviation and the column contributions kept in registers from j-1.  A
+// 4-slot ring keeps every slot a lagging peer may still read untouched.
+template <class T, int CH, int CL, int NT>
+__device__ __forceinline__ void pass_body_lag(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
+                                              const Slice &sl, RowXch<T, 1, CL> *xch, unsigned &xi) {
+    using V = typename VecT<T>::V;
+    constexpr int VW = VecT<T>::W;
+    constexpr int NW = NT / 32;
+    __shared__ T s_m[2][NW], s_s[2][NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = a.n;
+    const bool pre = (k == 0);
+    const bool rowonly = (k == max_sweeps + 1);
+    const double *gin = gslot(a, k + 1);
+    const double *fprev = fslot(a, k + 1);
+    double *fout = fslot(a, k);
+    const T *G = static_cast<const T *>(a.G);
+    const double ks = SkMath<T>::kScale;
+    const T coef = (T)(coef_d * ks);
+    const T gmax = (T)gmax_d;
+    const int c0 = sl.c0, c1 = sl.c1;
+    const bool writer = (sl.rank == 0);
+    const int nbands = n;
+
+    V xv[CH];
+    auto load_row = [&](int row, V (&dst)[CH]) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int col = c0 + (tid + NT * c) * VW;
+            if (row < n && col < c1)
+                dst[c] = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + col));
+            else
+                memset(&dst[c], 0, sizeof(V));
+        }
+    };
+    load_row(sl.grp, xv);
+    T gl[CH][VW], acc[CH][VW], xp[CH][VW];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+            const int col = c0 + (tid + NT * c) * VW + e;
+            const T gv = (!pre && col < c1) ? (T)(__ldcg(gin + col) * ks) : T(0);
+            gl[c][e] = col < c1 ? gv : neg_inf<T>();
+            acc[c][e] = T(0);
+            xp[c][e] = T(0);
+        }
+    double devmax = 0.0;
+    T mx_p = T(0), Mp = neg_inf<T>(), Sp = T(0);
+    double fprev_p = 0.0;
+    int row_p = -1;
+
+    // finish row row_p (band of exchange index jp) from the peers' pairs
+    auto finish = [&](unsigned jp) {
+        double lse = 0.0;
+        if (lane == 0) {
+            const int xs = jp & 3;
+            xbar_wait(&xch->bar[xs], (jp >> 2) & 1);
+            T mq[CL], sq[CL];
+#pragma unroll
+            for (int q = 0; q < CL; ++q) {
+                mq[q] = (q == sl.rank) ? Mp : xch->pair[xs][q][0][0];
+                sq[q] = (q == sl.rank) ? Sp : xch->pair[xs][q][0][1];
+            }
+            T M = neg_inf<T>();
+#pragma unroll
+            for (int q = 0; q < CL; ++q) M = mq[q] > M ? mq[q] : M;
+            T S = T(0);
+#pragma unroll
+            for (int q = 0; q < CL; ++q)
+                if (mq[q] != neg_inf<T>()) S += sq[q] * SkMath<T>::ex(mq[q] - M);
+            lse = (double)M + SkMath<T>::lgt(S);
+            if (writer && warp == 0 && row_p < n) {
+                const double fnew = -lse / ks;
+                double dev = 0.0;
+                if (pre) dev = SkMath<T>::dev(-fnew);
+                else if (k >= 2) dev = SkMath<T>::dev(fprev_p - fnew);
+                if (!pre) __stcg(fout + row_p, fnew);
+                devmax = fmax(devmax, dev);
+            }
+        }
+        lse = __shfl_sync(0xffffffffu, lse, 0);
+        if (!rowonly && row_p < n) {
+            const double colf = pre ? 0.0 : -lse;
+            const T sc = SkMath<T>::ex((T)((double)mx_p + colf));
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+                for (int e = 0; e < VW; ++e) acc[c][e] += xp[c][e] * sc;
+        }
+    };
+
+    int it = 0;
+    for (int row = sl.grp; row < nbands; row += sl.ngrp, ++it) {
+        T x[CH][VW];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const T *pv = reinterpret_cast<const T *>(&xv[c]);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) x[c][e] = pv[e];
+        }
+        load_row(row + sl.ngrp, xv);  // prefetch
+        double fpv = 0.0;
+        if (writer && warp == 0 && lane == 0 && k >= 2) fpv = __ldcg(fprev + row);
+        T m = neg_inf<T>();
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                const T arg = coef * (gmax - x[c][e]) + gl[c][e];
+                x[c][e] = arg;
+                m = arg > m ? arg : m;
+            }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const T m2 = __shfl_xor_sync(0xffffffffu, m, off);
+            m = m2 > m ? m2 : m;
+        }
+        const T mx = (m == neg_inf<T>()) ? T(0) : m;
+        T sum = T(0);
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                const T y = SkMath<T>::ex(x[c][e] - mx);
+                x[c][e] = y;
+                sum += y;
+            }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        const int par = it & 1;
+        if (lane == 0) { s_m[par][warp] = m; s_s[par][warp] = sum; }
+        __syncthreads();
+        T Mb = neg_inf<T>(), Sb = T(0);
+        if (lane == 0) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) { const T mw = s_m[par][w]; Mb = mw > Mb ? mw : Mb; }
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const T mw = s_m[par][w];
+                if (mw != neg_inf<T>()) Sb += s_s[par][w] * SkMath<T>::ex(mw - Mb);
+            }
+        }
+        const unsigned j = xi;
+        if (warp == 0 && lane == 0) {
+            const int xs = j & 3;
+            xbar_arm(&xch->bar[xs], (uint32_t)((CL - 1) * 2 * sizeof(T)));
+#pragma unroll
+            for (int q = 0; q < CL; ++q)
+                if (q != sl.rank)
+                    st_async_pair(dsmem_map(&xch->pair[xs][sl.rank][0][0], q), Mb, Sb, dsmem_map(&xch->bar[xs], q));
+        }
+        if (it > 0) finish(j - 1);
+        // this band becomes the pending one
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) xp[c][e] = x[c][e];
+        mx_p = mx;
+        Mp = Mb;
+        Sp = Sb;
+        fprev_p = fpv;
+        row_p = row;
+        ++xi;
+    }
+    if (it > 0) finish(xi - 1);
+    if (!rowonly) {
+        T *cp = static_cast<T *>(a.colpart) + (int64_t)sl.grp * a.ldp;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int col = c0 + (tid + NT * c) * VW;
+            if (col < c1) {
+                V v;
+                T *pv = reinterpret_cast<T *>(&v);
+#pragma unroll
+                for (int e = 0; e < VW; ++e) pv[e] = acc[c][e];
+                __stcg(reinterpret_cast<V *>(cp + col), v);
+            }
+        }
+    }
+    __shared__ double s_dev[NW];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) devmax = fmax(devmax, __shfl_xor_sync(0xffffffffu, devmax, off));
+    if (lane == 0) s_dev[warp] = devmax;
+    __syncthreads();
+    if (tid == 0) {
+        double d = 0.0;
+        for (int w = 0; w < NW; ++w) d = fmax(d, s_dev[w]);
+        __stcg(a.devpart + blockIdx.x, d);
         if (a.dslot) atomicMax(a.dslot + (k & 1), (unsigned long long)__double_as_longlong(d));
     }
 }
@@ -399,9 +596,9 @@ __device__ double sk_exact_col(const SkArgs &a, int j, const double *f, bool pre
 // ------------------------------------------------------------------ merge body
 // Columns [blk*256 + tid] strided by nblk*256.  On the pre-check writes this
 // CTA's max |colsum - 1| to devcol[blk].
-template <class T>
+template <class T, int NT>
 __device__ __forceinline__ void merge_body(const SkArgs &a, int k, double coef, double gmax, int blk, int nblk) {
-    constexpr int NW = kThreads / 32;
+    constexpr int NW = NT / 32;
     __shared__ double s_red[NW];
     const int tid = threadIdx.x, n = a.n, lane = tid & 31, warp = tid >> 5;
     const bool pre = (k == 0);
@@ -445,7 +642,7 @@ __device__ __forceinline__ void merge_body(const SkArgs &a, int k, double coef, 
         __syncthreads();
         if (tid == 0) {
             double d = 0.0;
-            for (int w = 0; w < kThreads / 32; ++w) d = fmax(d, s_red[w]);
+            for (int w = 0; w < NT / 32; ++w) d = fmax(d, s_red[w]);
             __stcg(a.devcol + blk, d);
             if (a.dslot) atomicMax(a.dslot + 2, (unsigned long long)__double_as_longlong(d));
         }
@@ -491,8 +688,8 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks, un
 }
 
 // ------------------------------------------------------------------ drivers
-template <class T, int CH, int R, int CL>
-__global__ void __launch_bounds__(kThreads, (CL > 1 ? 1 : 2)) sk_persistent_kernel(SkArgs a, unsigned *bar) {
+template <class T, int CH, int R, int CL, int NT>
+__global__ void __launch_bounds__(NT, (NT > 256 ? 1 : 2)) sk_persistent_kernel(SkArgs a, unsigned *bar) {
     __shared__ int s_k;
     if (threadIdx.x == 0) s_k = a.st->k;
     __syncthreads();
@@ -516,15 +713,15 @@ __global__ void __launch_bounds__(kThreads, (CL > 1 ? 1 : 2)) sk_persistent_kern
     unsigned xi = 0;  // exchange counter (bands processed by this cluster so far)
     if constexpr (CL > 1) {
         if (threadIdx.x == 0) {
-            xbar_init(&xch.bar[0]);
-            xbar_init(&xch.bar[1]);
+            for (int q = 0; q < 4; ++q) xbar_init(&xch.bar[q]);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         cluster_sync();  // every peer's barriers exist before the first st.async
     }
     unsigned epoch = 0;
     for (int k = k0;; ++k) {
-        pass_body<T, CH, R, CL>(a, k, K, coef, gmax, sl, &xch, xi);
+        if constexpr (CL > 1 && R == 1) pass_body_lag<T, CH, CL, NT>(a, k, K, coef, gmax, sl, &xch, xi);
+        else pass_body<T, CH, R, CL, NT>(a, k, K, coef, gmax, sl, &xch, xi);
         grid_barrier(bar, nblk, epoch);
         const double drow = __longlong_as_double((long long)__ldcg(a.dslot + (k & 1)));
         if (blk == 0 && threadIdx.x == 0) a.dslot[(k + 1) & 1] = 0ull;  // next sweep's slot
@@ -534,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, (CL > 1 ? 1 : 2)) sk_persistent_kern
             else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
         }
         if (!stop) {
-            merge_body<T>(a, k, coef, gmax, blk, nblk);
+            merge_body<T, NT>(a, k, coef, gmax, blk, nblk);
             grid_barrier(bar, nblk, epoch);
             if (k == 0) {
                 const double d0 = fmax(drow, __longlong_as_double((long long)__ldcg(a.dslot + 2)));
@@ -567,7 +764,7 @@ __global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
     if (s_done) return;
     const Slice sl{0, a.n, (int)blockIdx.x, (int)gridDim.x, 0};
     unsigned xi = 0;
-    pass_body<T, CH, R, 1>(a, s_k, a.st->max_sweeps, a.st->coef, a.st->gmax, sl, nullptr, xi);
+    pass_body<T, CH, R, 1, kThreads>(a, s_k, a.st->max_sweeps, a.st->coef, a.st->gmax, sl, nullptr, xi);
 }
 
 template <class T>
@@ -584,7 +781,7 @@ __global__ void __launch_bounds__(kThreads) sk_merge_kernel(SkArgs a) {
     const int K = a.st->max_sweeps;
     const double tol = a.st->tol;
     const bool pre = (k == 0);
-    if (k != K + 1) merge_body<T>(a, k, a.st->coef, a.st->gmax, blockIdx.x, gridDim.x);
+    if (k != K + 1) merge_body<T, kThreads>(a, k, a.st->coef, a.st->gmax, blockIdx.x, gridDim.x);
     if (tid == 0) {
         if (!pre) __stcg(a.devcol + blockIdx.x, 0.0);
         __threadfence();
@@ -670,43 +867,46 @@ __global__ void __launch_bounds__(kThreads) sk_emit_kernel(SkArgs a, T *Q, int64
 
 constexpr int kMaxCh = 8;
 constexpr int rows_for(int ch) { return ch == 1 ? 8 : ch == 2 ? 4 : ch <= 4 ? 2 : 1; }
-// Clustered (wide-row) kernels run one CTA per SM with more rows per band so the
-// per-band cluster barrier and reduction chain amortise over more bytes.
-constexpr int rows_for(int ch, int cl) { return cl == 1 ? rows_for(ch) : (ch <= 6 ? 4 : 2); }
+// Wide rows (n > 8192 fp32 / 4096 fp64) run 512-thread CTAs, one per SM:
+// half the chunks per thread, 16 warps to hide the reduction chains.
+constexpr int kWideThreads = 512;
+constexpr int rows_for(int ch, int nt) { return nt == kThreads ? rows_for(ch) : 1; }
 
-template <class T, int CH, int CL> void *persistent_fn() {
-    return (void *)sk_persistent_kernel<T, CH, rows_for(CH, CL), CL>;
+template <class T, int CH, int CL, int NT> void *persistent_fn() {
+    return (void *)sk_persistent_kernel<T, CH, rows_for(CH, NT), CL, NT>;
 }
 
-// CL == 1 for any CH; clusters only when one CTA cannot hold a row (CH of the slice >= 4).
-template <class T> void *persistent_for(int ch, int cl) {
-    if (cl == 1) {
+template <class T> void *persistent_for(int ch, int cl, int nt) {
+    if (nt == kThreads && cl == 1) {
         switch (ch) {
-            case 1: return persistent_fn<T, 1, 1>();
-            case 2: return persistent_fn<T, 2, 1>();
-            case 3: return persistent_fn<T, 3, 1>();
-            case 4: return persistent_fn<T, 4, 1>();
-            case 5: return persistent_fn<T, 5, 1>();
-            case 6: return persistent_fn<T, 6, 1>();
-            case 7: return persistent_fn<T, 7, 1>();
-            case 8: return persistent_fn<T, 8, 1>();
+            case 1: return persistent_fn<T, 1, 1, kThreads>();
+            case 2: return persistent_fn<T, 2, 1, kThreads>();
+            case 3: return persistent_fn<T, 3, 1, kThreads>();
+            case 4: return persistent_fn<T, 4, 1, kThreads>();
+            case 5: return persistent_fn<T, 5, 1, kThreads>();
+            case 6: return persistent_fn<T, 6, 1, kThreads>();
+            case 7: return persistent_fn<T, 7, 1, kThreads>();
+            case 8: return persistent_fn<T, 8, 1, kThreads>();
         }
     }
-#define GOAT_CL(C)                                         \
-    if (cl == C) {                                         \
-        switch (ch) {                                      \
-            case 4: return persistent_fn<T, 4, C>();       \
-            case 5: return persistent_fn<T, 5, C>();       \
-            case 6: return persistent_fn<T, 6, C>();       \
-            case 7: return persistent_fn<T, 7, C>();       \
-            case 8: return persistent_fn<T, 8, C>();       \
-        }                                                  \
+#define GOAT_CL(C)                                                   \
+    if (nt == kWideThreads && cl == C) {                             \
+        switch (ch) {                                                \
+            case 3: return persistent_fn<T, 3, C, kWideThreads>();   \
+            case 4: return persistent_fn<T, 4, C, kWideThreads>();   \
+            case 5: return persistent_fn<T, 5, C, kWideThreads>();   \
+            case 6: return persistent_fn<T, 6, C, kWideThreads>();   \
+            case 7: return persistent_fn<T, 7, C, kWideThreads>();   \
+            case 8: return persistent_fn<T, 8, C, kWideThreads>();   \
+        }                                                            \
     }
+    GOAT_CL(1)
     GOAT_CL(2)
     GOAT_CL(4)
     GOAT_CL(8)
 #undef GOAT_CL
-    throw Error(GOAT_ENOTSUP, "sinkhorn: no kernel for chunks=" + std::to_string(ch) + " cluster=" + std::to_string(cl));
+    throw Error(GOAT_ENOTSUP, "sinkhorn: no kernel for chunks=" + std::to_string(ch) + " cluster=" +
+                                  std::to_string(cl) + " threads=" + std::to_string(nt));
 }
 
 int env_int(const char *name, int dflt) {
@@ -717,7 +917,7 @@ int env_int(const char *name, int dflt) {
 cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunchAttribute (&attrs)[2]) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.nblk);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(p.nt);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     attrs[0].id = cudaLaunchAttributeCooperative;
@@ -742,23 +942,29 @@ template <class T> SkPlan sk_plan(int n, int num_sms) {
     // Row width per CTA: whole rows when they fit kMaxCh chunks per thread,
     // else a cluster of cl CTAs splits each row into column slices.
     p.cl = 1;
+    p.nt = kThreads;
     p.slice_w = (int)round_up(n, 8 * VW);
     p.ch = ceil_div(ceil_div(n, VW), kThreads);
-    while (p.ch > kMaxCh && p.cl < 8) {
-        p.cl *= 2;
-        p.slice_w = (int)round_up(ceil_div(n, p.cl), 8 * VW);
-        p.ch = std::max(4, ceil_div(ceil_div(p.slice_w, VW), kThreads));
+    if (p.ch > kMaxCh) {
+        // wide rows: 512-thread CTAs, then clusters of 2/4/8 splitting the row
+        p.nt = kWideThreads;
+        p.ch = std::max(3, ceil_div(ceil_div(n, VW), kWideThreads));
+        while (p.ch > kMaxCh && p.cl < 8) {
+            p.cl *= 2;
+            p.slice_w = (int)round_up(ceil_div(n, p.cl), 8 * VW);
+            p.ch = std::max(3, ceil_div(ceil_div(p.slice_w, VW), kWideThreads));
+        }
     }
     if (p.ch > kMaxCh)
         throw Error(GOAT_ENOTSUP, "sinkhorn: order " + std::to_string(n) + " exceeds 8-CTA clusters of this build");
-    p.rows = rows_for(p.ch, p.cl);
+    p.rows = rows_for(p.ch, p.nt);
     const int nbands = (n + p.rows - 1) / p.rows;
-    p.persistent = env_int("GOAT_SK_PERSISTENT", 1) != 0 || p.cl > 1;
+    p.persistent = env_int("GOAT_SK_PERSISTENT", 1) != 0 || p.nt != kThreads;
     // Co-resident groups (CTAs, or clusters of cl CTAs) for the cooperative launch.
     int groups = 0;
     if (p.cl == 1) {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)persistent_for<T>(p.ch, 1), kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)persistent_for<T>(p.ch, 1, p.nt), p.nt, 0);
         groups = std::max(1, occ) * num_sms;  // measured: all co-resident CTAs is fastest (n <= 5000)
     } else {
         cudaLaunchAttribute attrs[2];
@@ -770,7 +976,7 @@ template <class T> SkPlan sk_plan(int n, int num_sms) {
         cfg.attrs = &cattr;
         cfg.numAttrs = 1;
         int ncl = 0;
-        GOAT_CUDA(cudaOccupancyMaxActiveClusters(&ncl, persistent_for<T>(p.ch, p.cl), &cfg));
+        GOAT_CUDA(cudaOccupancyMaxActiveClusters(&ncl, persistent_for<T>(p.ch, p.cl, p.nt), &cfg));
         groups = std::max(1, ncl);
     }
     int ngrp = std::max(1, std::min(nbands, groups));
@@ -790,7 +996,7 @@ void launch_pass_ch(const SkArgs &a, const SkPlan &p, cudaStream_t s) {
 }
 
 template <class T> void sk_launch_pass(const SkArgs &a, const SkPlan &p, cudaStream_t s) {
-    if (p.cl != 1) throw Error(GOAT_ENOTSUP, "sinkhorn: cluster-split rows need the persistent driver");
+    if (p.cl != 1 || p.nt != kThreads) throw Error(GOAT_ENOTSUP, "sinkhorn: wide rows need the persistent driver");
     switch (p.ch) {
         case 1: launch_pass_ch<T, 1>(a, p, s); break;
         case 2: launch_pass_ch<T, 2>(a, p, s); break;
@@ -820,7 +1026,7 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
     void *params[] = {&args, &bar};
     cudaLaunchAttribute attrs[2];
     cudaLaunchConfig_t cfg = persistent_config(p, s, attrs);
-    GOAT_CUDA(cudaLaunchKernelExC(&cfg, persistent_for<T>(p.ch, p.cl), params));
+    GOAT_CUDA(cudaLaunchKernelExC(&cfg, persistent_for<T>(p.ch, p.cl, p.nt), params));
     note_launch();
 }
 

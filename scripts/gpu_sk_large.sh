@@ -1,2 +1,2 @@
-for n in 1000 5000 40000; do python scripts/prof_sweep.py $n fp32 20; done
-timeout 900 python -m pytest tests/ -q -m gpu -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log; grep FAILED gpurun_out/pytest_gpu.log | head
+for n in 5000 10000 20000 40000; do python scripts/prof_sweep.py $n fp32 20; done
+timeout 900 python -m pytest tests/ -q -m gpu -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log; grep FAILED gpurun_out/pytest_gpu.log | head
