@@ -60,6 +60,10 @@ template <> struct SkMath<double> {
     __device__ static double dev(double d) { return fabs(expm1(d)); }
 };
 
+// max without NaN handling (arguments are never NaN): one FMNMX
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
+
 template <class T> __device__ __forceinline__ T neg_inf();
 template <> __device__ __forceinline__ float neg_inf<float>() { return -INFINITY; }
 template <> __device__ __forceinline__ double neg_inf<double>() { return -INFINITY; }
@@ -231,7 +235,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
                 for (int e = 0; e < VW; ++e) {
                     const T arg = coef * (gmax - x[r][c][e]) + gl[c][e];  // E_ij + g_j (sinkhorn.py:125)
                     x[r][c][e] = arg;
-                    m[r] = arg > m[r] ? arg : m[r];
+                    m[r] = vmax(m[r], arg);
                 }
         }
         // Warp max first (shuffle + max only), then exponentials against the warp
@@ -251,15 +255,20 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            s[r] = T(0);
+            T sp[VW];  // VW independent partial sums (short add chains)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) sp[e] = T(0);
 #pragma unroll
             for (int c = 0; c < CH; ++c)
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
                     const T y = SkMath<T>::ex(x[r][c][e] - mx[r]);
                     x[r][c][e] = y;
-                    s[r] += y;
+                    sp[e] += y;
                 }
+            s[r] = T(0);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) s[r] += sp[e];
             if (m[r] == neg_inf<T>()) s[r] = T(0);
         }
 #pragma unroll
@@ -276,14 +285,33 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
             for (int r = 0; r < R; ++r) { s_m[par][warp][r] = m[r]; s_s[par][warp][r] = s[r]; }
         }
         __syncthreads();
+        // Cross-warp combine, lane-parallel: lane = (row rr, warp w) with NW lanes per
+        // row; max butterfly, one exponential per lane, sum butterfly (fixed xor
+        // trees: deterministic, identical in every warp).  Lane rr*NW holds row rr.
         T Mb = neg_inf<T>(), Sb = T(0);
-        if (lane < R) {
+        {
+            constexpr int RL = 32 / NW;  // rows combined per warp pass
 #pragma unroll
-            for (int w = 0; w < NW; ++w) { const T mw = s_m[par][w][lane]; Mb = mw > Mb ? mw : Mb; }
+            for (int rb = 0; rb < R; rb += RL) {
+                const int rr = rb + lane / NW, w = lane % NW;
+                const bool ok = rr < R;
+                const T mw = ok ? s_m[par][w][ok ? rr : 0] : neg_inf<T>();
+                T M = mw;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                const T mw = s_m[par][w][lane];
-                if (mw != neg_inf<T>()) Sb += s_s[par][w][lane] * SkMath<T>::ex(mw - Mb);
+                for (int off = NW / 2; off > 0; off >>= 1) {
+                    const T m2 = __shfl_xor_sync(0xffffffffu, M, off);
+                    M = m2 > M ? m2 : M;
+                }
+                T S = (mw != neg_inf<T>()) ? s_s[par][w][ok ? rr : 0] * SkMath<T>::ex(mw - M) : T(0);
+#pragma unroll
+                for (int off = NW / 2; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+                // move row (rb + lane)'s result to lane (rb + lane) - rb ... i.e. lane r <- row r
+#pragma unroll
+                for (int q = 0; q < RL; ++q) {
+                    const T Mq = __shfl_sync(0xffffffffu, M, q * NW);
+                    const T Sq = __shfl_sync(0xffffffffu, S, q * NW);
+                    if (lane == rb + q) { Mb = Mq; Sb = Sq; }
+                }
             }
         }
         if constexpr (CL > 1) {
@@ -324,7 +352,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
             lse_l = (double)Mb + SkMath<T>::lgt(Sb);  // scaled units
             const int row = r0 + lane;
             if (writer && warp == 0 && row < n) {
-                const double fnew = -lse_l / ks;
+                const double fnew = -lse_l * (1.0 / SkMath<T>::kScale);
                 double dev = 0.0;
                 if (pre) dev = SkMath<T>::dev(-fnew);                  // |rowsum(K) - 1|
                 else if (k >= 2) dev = SkMath<T>::dev(fprev_v - fnew);  // |u K v - 1|
@@ -455,7 +483,7 @@ __device__ __forceinline__ void pass_body_lag(const SkArgs &a, int k, int max_sw
                 if (mq[q] != neg_inf<T>()) S += sq[q] * SkMath<T>::ex(mq[q] - M);
             lse = (double)M + SkMath<T>::lgt(S);
             if (writer && warp == 0 && row_p < n) {
-                const double fnew = -lse / ks;
+                const double fnew = -lse * (1.0 / SkMath<T>::kScale);
                 double dev = 0.0;
                 if (pre) dev = SkMath<T>::dev(-fnew);
                 else if (k >= 2) dev = SkMath<T>::dev(fprev_p - fnew);
@@ -493,7 +521,7 @@ __device__ __forceinline__ void pass_body_lag(const SkArgs &a, int k, int max_sw
             for (int e = 0; e < VW; ++e) {
                 const T arg = coef * (gmax - x[c][e]) + gl[c][e];
                 x[c][e] = arg;
-                m = arg > m ? arg : m;
+                m = vmax(m, arg);
             }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
@@ -501,29 +529,40 @@ __device__ __forceinline__ void pass_body_lag(const SkArgs &a, int k, int max_sw
             m = m2 > m ? m2 : m;
         }
         const T mx = (m == neg_inf<T>()) ? T(0) : m;
-        T sum = T(0);
+        T sp[VW];  // VW independent partial sums (short add chains)
+#pragma unroll
+        for (int e = 0; e < VW; ++e) sp[e] = T(0);
 #pragma unroll
         for (int c = 0; c < CH; ++c)
 #pragma unroll
             for (int e = 0; e < VW; ++e) {
                 const T y = SkMath<T>::ex(x[c][e] - mx);
                 x[c][e] = y;
-                sum += y;
+                sp[e] += y;
             }
+        T sum = T(0);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) sum += sp[e];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
         const int par = it & 1;
         if (lane == 0) { s_m[par][warp] = m; s_s[par][warp] = sum; }
         __syncthreads();
-        T Mb = neg_inf<T>(), Sb = T(0);
-        if (lane == 0) {
+        // lane-parallel cross-warp combine (lane w holds warp w's pair); result in lane 0
+        T Mb, Sb;
+        {
+            const T mw = lane < NW ? s_m[par][lane] : neg_inf<T>();
+            T M = mw;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) { const T mw = s_m[par][w]; Mb = mw > Mb ? mw : Mb; }
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                const T mw = s_m[par][w];
-                if (mw != neg_inf<T>()) Sb += s_s[par][w] * SkMath<T>::ex(mw - Mb);
+            for (int off = NW / 2; off > 0; off >>= 1) {
+                const T m2 = __shfl_xor_sync(0xffffffffu, M, off);
+                M = m2 > M ? m2 : M;
             }
+            T S = (mw != neg_inf<T>()) ? s_s[par][lane] * SkMath<T>::ex(mw - M) : T(0);
+#pragma unroll
+            for (int off = NW / 2; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+            Mb = M;
+            Sb = S;
         }
         const unsigned j = xi;
         if (warp == 0 && lane == 0) {
