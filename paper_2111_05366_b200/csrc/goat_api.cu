@@ -43,11 +43,13 @@ struct Handle {
     DevBuf A64, B64, stage;                     // fp64 inputs (objective) + upload staging
     DevBuf f[2], g[2], colpart, devpart, devcol, state, red, scal, vec, ivec;
     DevBuf lap_d[3], lap_i[4], lap_b[2], lap_misc, bar;
+    DevBuf auc_d[2], auc_i[4], auc_u64, auc_misc;  // auction LAP state
     // tcgen05 path: bf16 planes of A, A^T, the first-GEMM operand ([B] or [B; B^T]),
     // the iterate X and the intermediate Y^T.
     DevBuf tcA, tcAt, tcB, tcX, tcY, tcS;
     int tc_na = 0, tc_nb = 0;  // planes of A / B (1 when exact in bf16)
     double *h_scal = nullptr;                   // pinned host scalars
+    int lap_stats[4] = {0, 0, 0, 0};            // last auction: assigned, rounds, capped, freed
     SkState *h_state = nullptr;                 // pinned
     ~Handle() {
         if (h_scal) cudaFreeHost(h_scal);
@@ -60,6 +62,10 @@ namespace {
 
 
 inline int64_t ld_for(int64_t n) { return round_up(std::max<int64_t>(n, 1), 8); }
+
+// Below this order the scipy-visiting-order solver runs from scratch (its
+// assignments match scipy even under ties); above it the auction front end.
+constexpr int kAuctionMinN = 256;
 
 void ensure_workspace(Handle &h, int64_t n) {
     GOAT_CUDA(cudaSetDevice(h.device));
@@ -390,7 +396,32 @@ int run_lap(Ctx &c, const T *M, int sense, int *perm_dev, std::vector<int> &perm
         w.col4row = perm_dev; w.rem = h.lap_i[2].as<int>();
         w.SR = h.lap_b[0].as<unsigned char>(); w.SC = h.lap_b[1].as<unsigned char>();
         w.status = flag + 4;
-        launch_lap_sap<T>(M, c.ld, n, sense, w, c.s);
+        int warm = 0;
+        const char *ae = getenv("GOAT_LAP_AUCTION");
+        if (n >= kAuctionMinN && !(ae && atoi(ae) == 0)) {
+            // eps-scaling auction, then certified repair by warm-started augmenting paths
+            double *mm = h.scal.as<double>() + 48;
+            launch_minmax<T>(M, c.ld, n, h.red.as<double>(), mm, c.s);
+            double lohi[2];
+            GOAT_CUDA(cudaMemcpyAsync(lohi, mm, 16, cudaMemcpyDeviceToHost, c.s));
+            sync(c);
+            const size_t vb = (size_t)n * 8, ib = (size_t)n * 4;
+            for (int q = 0; q < 2; ++q) h.auc_d[q].ensure(vb);
+            for (int q = 0; q < 4; ++q) h.auc_i[q].ensure(ib);
+            h.auc_u64.ensure(vb);
+            h.auc_misc.ensure(512);
+            AuctionWork aw{};
+            aw.price = h.auc_d[0].as<double>(); aw.row_bid_v = h.auc_d[1].as<double>();
+            aw.row_col = h.auc_i[0].as<int>(); aw.col_row = h.auc_i[1].as<int>();
+            aw.bid_row = h.auc_i[2].as<int>(); aw.row_bid = h.auc_i[3].as<int>();
+            aw.bid_val = h.auc_u64.as<unsigned long long>();
+            aw.counters = h.auc_misc.as<int>();
+            aw.bar = reinterpret_cast<unsigned *>(h.auc_misc.as<char>() + 256);
+            launch_lap_auction<T>(M, c.ld, n, sense, lohi[1] - lohi[0], w, aw, h.num_sms, c.s);
+            GOAT_CUDA(cudaMemcpyAsync(h.lap_stats, aw.counters, 16, cudaMemcpyDeviceToHost, c.s));
+            warm = 1;
+        }
+        launch_lap_sap<T>(M, c.ld, n, sense, w, c.s, warm);
         int status = 0;
         GOAT_CUDA(cudaMemcpyAsync(&status, w.status, sizeof(int), cudaMemcpyDeviceToHost, c.s));
         sync(c);

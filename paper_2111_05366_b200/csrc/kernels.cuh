@@ -106,6 +106,18 @@ struct LapWork {
     int *status;
 };
 template <class T>
-void launch_lap_sap(const T *M, int64_t ld, int n, int sense, const LapWork &w, cudaStream_t s);
+void launch_lap_sap(const T *M, int64_t ld, int n, int sense, const LapWork &w, cudaStream_t s, int warm = 0);
+// eps-scaling auction + exact-repair preparation (lap.cu): fills w.u, w.v,
+// w.row4col, w.col4row with a tight partial assignment and feasible duals for a
+// warm-started launch_lap_sap.  counters: [0] assigned, [1] rounds, [2] capped, [3] freed rows.
+struct AuctionWork {
+    double *price, *row_bid_v;
+    int *row_col, *col_row, *bid_row, *row_bid, *counters;
+    unsigned long long *bid_val;
+    unsigned *bar;
+};
+template <class T>
+int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, const LapWork &w,
+                       const AuctionWork &aw, int num_sms, cudaStream_t s);
 
 }  // namespace goat

@@ -14,6 +14,7 @@
 //    scan and argmin parallel across 1024 threads.  Identical fp64 operations in
 //    identical order give scipy's assignment bit-for-bit, ties included.
 //    No CPU fallback exists.
+#include <algorithm>
 #include <climits>
 
 #include "kernels.cuh"
@@ -75,7 +76,7 @@ constexpr int kLapThreads = 1024;
 
 template <class T>
 __global__ void __launch_bounds__(kLapThreads, 1)
-    lap_sap_kernel(const T *M, int64_t ld, int n, double sign, LapWork w, int use_smem) {
+    lap_sap_kernel(const T *M, int64_t ld, int n, double sign, LapWork w, int use_smem, int warm) {
     extern __shared__ __align__(16) unsigned char smem[];
     double *spc = w.spc, *v = w.v;
     int *path = w.path, *row4col = w.row4col, *rem = w.rem;
@@ -96,11 +97,19 @@ __global__ void __launch_bounds__(kLapThreads, 1)
     __shared__ double s_minv;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    for (int j = tid; j < n; j += kLapThreads) {
-        v[j] = 0.0; u[j] = 0.0; row4col[j] = -1; col4row[j] = -1; path[j] = -1;
+    if (warm) {
+        // warm start (auction repair): tight partial assignment + feasible duals given
+        for (int j = tid; j < n; j += kLapThreads) {
+            v[j] = w.v[j]; row4col[j] = w.row4col[j]; path[j] = -1;
+        }
+    } else {
+        for (int j = tid; j < n; j += kLapThreads) {
+            v[j] = 0.0; u[j] = 0.0; row4col[j] = -1; col4row[j] = -1; path[j] = -1;
+        }
     }
     __syncthreads();
     for (int cur = 0; cur < n; ++cur) {
+        if (warm && col4row[cur] != -1) continue;  // already assigned (uniform: global, synced)
         for (int it = tid; it < n; it += kLapThreads) {
             rem[it] = n - 1 - it; SR[it] = 0; SC[it] = 0; spc[it] = INFINITY;
         }
@@ -176,7 +185,192 @@ __global__ void __launch_bounds__(kLapThreads, 1)
     if (tid == 0) *w.status = 0;
 }
 
+
+// ------------------------------------------------------------------ auction
+// Forward auction with epsilon scaling (Bertsekas) for large n, as the fast
+// front end of the exact solver: warps bid for unassigned rows (best and
+// second-best of val_ij - p_j over all columns), columns take the highest bid
+// (atomicMax on the bit pattern of non-negative doubles, ties to the lowest
+// row), prices rise to the winning bid.  One cooperative launch runs every
+// phase; the result is eps-optimal, and lap_auction_repair + the warm-started
+// augmenting-path kernel turn it into a certified exact optimum.
+struct AucArgs {
+    int n;
+    int64_t ld;
+    double sign;           // val = sign * M  (+1 maximize, -1 minimize)
+    double eps0, eps_min, theta;
+    double *price;         // [n]
+    int *row_col;          // [n] column of row (-1)
+    int *col_row;          // [n] row of column (-1)
+    unsigned long long *bid_val;  // [n] highest bid on column (bits), 0 = none
+    int *bid_row;          // [n] winning row (INT_MAX = none)
+    int *row_bid;          // [n] column this row bid on this round (-1)
+    double *row_bid_v;     // [n]
+    unsigned *bar;         // grid barrier counter (zeroed)
+    int *counters;         // [0] assigned columns, [1] rounds (diagnostic), [2] status
+    int max_rounds;
+};
+
+__device__ __forceinline__ unsigned ld_acq(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void gbar(unsigned *bar, unsigned nb, unsigned &epoch) {
+    ++epoch;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(bar), "r"(1u) : "memory");
+        while (ld_acq(bar) < epoch * nb) { }
+    }
+    __syncthreads();
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a) {
+    const int n = a.n, lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    unsigned epoch = 0;
+    __shared__ int s_done;
+    int rounds = 0;
+    for (double eps = a.eps0;; eps = fmax(eps / a.theta, a.eps_min)) {
+        // new phase: empty assignment, prices kept
+        for (int j = gt; j < n; j += nt) { a.row_col[j] = -1; a.col_row[j] = -1; a.bid_val[j] = 0ull; a.bid_row[j] = INT_MAX; a.row_bid[j] = -1; }
+        if (gt == 0) a.counters[0] = 0;
+        gbar(a.bar, gridDim.x, epoch);
+        for (;;) {
+            // (A) bids of unassigned rows
+            for (int i = gw; i < n; i += nwarps) {
+                if (__ldcg(a.row_col + i) != -1) continue;
+                const T *Mi = M + (int64_t)i * a.ld;
+                double w1 = -INFINITY, w2 = -INFINITY;
+                int j1 = INT_MAX;
+                for (int j = lane; j < n; j += 32) {
+                    const double v = a.sign * (double)Mi[j] - __ldcg(a.price + j);
+                    if (v > w1) { w2 = w1; w1 = v; j1 = j; }
+                    else if (v > w2) w2 = v;
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double b1 = __shfl_xor_sync(0xffffffffu, w1, off);
+                    const double b2 = __shfl_xor_sync(0xffffffffu, w2, off);
+                    const int bj = __shfl_xor_sync(0xffffffffu, j1, off);
+                    if (b1 > w1 || (b1 == w1 && bj < j1)) {
+                        w2 = fmax(b2, w1);
+                        w1 = b1;
+                        j1 = bj;
+                    } else {
+                        w2 = fmax(w2, b1);
+                    }
+                }
+                if (lane == 0) {
+                    const double gap = (w2 == -INFINITY) ? 0.0 : (w1 - w2);
+                    const double bid = __ldcg(a.price + j1) + gap + eps;
+                    a.row_bid[i] = j1;
+                    a.row_bid_v[i] = bid;
+                    atomicMax(a.bid_val + j1, (unsigned long long)__double_as_longlong(bid));
+                }
+            }
+            gbar(a.bar, gridDim.x, epoch);
+            // (B) ties on the winning bid go to the lowest row
+            for (int i = gt; i < n; i += nt) {
+                const int j = __ldcg(a.row_bid + i);
+                if (j >= 0 && (unsigned long long)__double_as_longlong(__ldcg(a.row_bid_v + i)) == __ldcg(a.bid_val + j))
+                    atomicMin(a.bid_row + j, i);
+            }
+            gbar(a.bar, gridDim.x, epoch);
+            // (C) columns take their winner; evicted owners become unassigned
+            for (int j = gt; j < n; j += nt) {
+                const unsigned long long bv = __ldcg(a.bid_val + j);
+                if (bv == 0ull) continue;
+                const int w = __ldcg(a.bid_row + j);
+                const int old = __ldcg(a.col_row + j);
+                if (old >= 0) a.row_col[old] = -1;
+                else atomicAdd(a.counters, 1);
+                a.col_row[j] = w;
+                a.row_col[w] = j;
+                a.price[j] = __longlong_as_double((long long)bv);
+                a.bid_val[j] = 0ull;
+                a.bid_row[j] = INT_MAX;
+            }
+            for (int i = gt; i < n; i += nt) a.row_bid[i] = -1;
+            gbar(a.bar, gridDim.x, epoch);
+            ++rounds;
+            if (threadIdx.x == 0) s_done = (__ldcg(a.counters) >= n) || rounds >= a.max_rounds;
+            __syncthreads();
+            if (s_done) break;
+        }
+        if (eps <= a.eps_min || rounds >= a.max_rounds) break;
+    }
+    if (gt == 0) { a.counters[1] = rounds; a.counters[2] = (rounds >= a.max_rounds) ? 1 : 0; }
+}
+
+// Exact-repair preparation: duals from the auction prices in the minimisation
+// form of the augmenting-path solver (cost c = -val, v_j = -p_j,
+// u_i = min_j c_ij - v_j); rows whose column is not an exact argmin are freed.
+template <class T>
+__global__ void lap_auction_repair(const T *M, AucArgs a, double *u, double *v, int *row4col, int *col4row, int *nfree) {
+    const int n = a.n, lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int i = gw; i < n; i += nwarps) {
+        const T *Mi = M + (int64_t)i * a.ld;
+        double best = -INFINITY;
+        for (int j = lane; j < n; j += 32) best = fmax(best, a.sign * (double)Mi[j] - a.price[j]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
+        if (lane == 0) {
+            u[i] = -best;
+            const int j = a.row_col[i];
+            const bool tight = j >= 0 && (a.sign * (double)Mi[j] - a.price[j]) == best;
+            col4row[i] = tight ? j : -1;
+            if (!tight) atomicAdd(nfree, 1);
+        }
+    }
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        v[j] = -a.price[j];
+        const int r = a.col_row[j];
+        const bool keep = r >= 0 && a.row_col[r] == j;
+        row4col[j] = keep ? r : -1;
+    }
+}
+
+// Drop columns whose row was freed (second pass: col4row is final).
+__global__ void lap_auction_unlink(int n, const int *col4row, int *row4col) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int r = row4col[j];
+        if (r >= 0 && col4row[r] != j) row4col[j] = -1;
+    }
+}
+
 }  // namespace
+
+template <class T>
+int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, const LapWork &w,
+                       const AuctionWork &aw, int num_sms, cudaStream_t s) {
+    AucArgs a{};
+    a.n = n; a.ld = ld; a.sign = (sense == GOAT_MAXIMIZE) ? 1.0 : -1.0;
+    a.eps0 = std::max(range, 1e-300) / 4.0;
+    a.eps_min = std::max(range, 1e-300) * 1e-7 / std::max(n, 1);
+    a.theta = 8.0;
+    a.price = aw.price; a.row_col = aw.row_col; a.col_row = aw.col_row; a.bid_val = aw.bid_val;
+    a.bid_row = aw.bid_row; a.row_bid = aw.row_bid; a.row_bid_v = aw.row_bid_v; a.bar = aw.bar;
+    a.counters = aw.counters; a.max_rounds = 200000;
+    GOAT_CUDA(cudaMemsetAsync(aw.price, 0, sizeof(double) * n, s));
+    GOAT_CUDA(cudaMemsetAsync(aw.bar, 0, 256, s));
+    GOAT_CUDA(cudaMemsetAsync(aw.counters, 0, 16, s));
+    int occ = 0;
+    GOAT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lap_auction_kernel<T>, 256, 0));
+    const int grid = std::max(1, occ) * num_sms;
+    void *params[] = {(void *)&M, &a};
+    GOAT_CUDA(cudaLaunchCooperativeKernel((const void *)lap_auction_kernel<T>, dim3(grid), dim3(256), params, 0, s));
+    note_launch();
+    lap_auction_repair<T><<<num_sms * 4, 256, 0, s>>>(M, a, w.u, w.v, w.row4col, w.col4row, aw.counters + 3); note_launch();
+    lap_auction_unlink<<<std::max(1, std::min(ceil_div(n, 256), num_sms * 4)), 256, 0, s>>>(n, w.col4row, w.row4col); note_launch();
+    GOAT_CHECK_LAUNCH();
+    return 0;
+}
 
 template <class T>
 void launch_lap_certificate(const T *M, int64_t ld, int n, int sense, int *cand, int *hits, int *flag,
@@ -192,19 +386,23 @@ void launch_lap_certificate(const T *M, int64_t ld, int n, int sense, int *cand,
 }
 
 template <class T>
-void launch_lap_sap(const T *M, int64_t ld, int n, int sense, const LapWork &w, cudaStream_t s) {
+void launch_lap_sap(const T *M, int64_t ld, int n, int sense, const LapWork &w, cudaStream_t s, int warm) {
     const size_t smem = (size_t)n * (8 + 8 + 4 + 4 + 4 + 1) + 16;
     int use_smem = smem <= 200 * 1024;
     if (use_smem)
         GOAT_CUDA(cudaFuncSetAttribute(lap_sap_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const double sign = (sense == GOAT_MAXIMIZE) ? -1.0 : 1.0;
-    lap_sap_kernel<T><<<1, kLapThreads, use_smem ? smem : 0, s>>>(M, ld, n, sign, w, use_smem); note_launch();
+    lap_sap_kernel<T><<<1, kLapThreads, use_smem ? smem : 0, s>>>(M, ld, n, sign, w, use_smem, warm); note_launch();
     GOAT_CHECK_LAUNCH();
 }
 
+template int launch_lap_auction<float>(const float *, int64_t, int, int, double, const LapWork &, const AuctionWork &, int,
+                                       cudaStream_t);
+template int launch_lap_auction<double>(const double *, int64_t, int, int, double, const LapWork &,
+                                        const AuctionWork &, int, cudaStream_t);
 template void launch_lap_certificate<float>(const float *, int64_t, int, int, int *, int *, int *, cudaStream_t);
 template void launch_lap_certificate<double>(const double *, int64_t, int, int, int *, int *, int *, cudaStream_t);
-template void launch_lap_sap<float>(const float *, int64_t, int, int, const LapWork &, cudaStream_t);
-template void launch_lap_sap<double>(const double *, int64_t, int, int, const LapWork &, cudaStream_t);
+template void launch_lap_sap<float>(const float *, int64_t, int, int, const LapWork &, cudaStream_t, int);
+template void launch_lap_sap<double>(const double *, int64_t, int, int, const LapWork &, cudaStream_t, int);
 
 }  // namespace goat
