@@ -876,6 +876,7 @@ int goat_set_stream(goat_handle *h, void *stream) {
 int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int32_t reps, double *ms_per_sweep) {
     return guarded([&] {
         require(h && dG && ms_per_sweep && reps >= 1, "bad argument");
+        require(ld >= n && ld % 8 == 0 && ((uintptr_t)dG & 15) == 0, "bench_sweep: ld must be a multiple of 8, G 16-byte aligned");
         check_order(n);
         ensure_workspace(*h, n);
         dispatch(*h, [&](auto *tag) {
@@ -913,6 +914,31 @@ int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int3
                 }
             };
             run();  // warm
+            if (const char *tk = getenv("GOAT_SK_TRACE")) {
+                // diagnostics: per-CTA phase stamps of one sweep, summarised on stderr
+                const int nb = plan.nblk;
+                DevBuf tb;
+                tb.ensure((size_t)nb * 16 * sizeof(unsigned long long));
+                GOAT_CUDA(cudaMemsetAsync(tb.p, 0, (size_t)nb * 128, c.s));
+                a.trace = tb.as<unsigned long long>();
+                a.trace_k = atoi(tk);
+                run();
+                GOAT_CUDA(cudaStreamSynchronize(c.s));
+                std::vector<unsigned long long> t((size_t)nb * 16);
+                GOAT_CUDA(cudaMemcpy(t.data(), tb.p, t.size() * 8, cudaMemcpyDeviceToHost));
+                unsigned long long t0 = ~0ull;
+                for (int b = 0; b < nb; ++b) if (t[b * 16]) t0 = std::min(t0, t[b * 16]);
+                fprintf(stderr, "sk_trace n=%d nblk=%d cl=%d stages=%d (ns after first pass start): stamp min/median/max\n", (int)n, nb, plan.cl, plan.stages);
+                for (int i = 0; i < 16; ++i) {
+                    std::vector<double> v;
+                    for (int b = 0; b < nb; ++b) if (t[b * 16 + i]) v.push_back((double)(t[b * 16 + i] - t0));
+                    if (v.empty()) continue;
+                    std::sort(v.begin(), v.end());
+                    fprintf(stderr, "  stamp %d: %8.0f %8.0f %8.0f\n", i, v.front(), v[v.size() / 2], v.back());
+                }
+                a.trace = nullptr;
+                a.trace_k = -1;
+            }
             cudaEvent_t e0, e1;
             GOAT_CUDA(cudaEventCreate(&e0));
             GOAT_CUDA(cudaEventCreate(&e1));

@@ -22,6 +22,11 @@ struct SkArgs {
     int nblk;           // CTAs of the pass kernel
     unsigned long long *dslot = nullptr;  // persistent driver: atomicMax dev slots [row k&1 | col]
     int slice_w = 0;    // cluster-split rows: columns per CTA rank
+    int resident = 1;   // keep a CTA's single band in registers across sweeps
+    int stages = 0;     // wide rows: shared-memory ring stages (0 = register path)
+    unsigned long long *trace = nullptr;  // diagnostics: per-CTA phase timestamps of sweep trace_k
+    int trace_k = -1;
+    int stage_bytes = 0;
 };
 
 struct SkPlan {
@@ -35,6 +40,9 @@ struct SkPlan {
     int ngrp = 0;             // row groups (= nblk / cl)
     int slice_w = 0;          // columns per CTA rank when cl > 1
     size_t colpart_bytes = 0;
+    int stages = 0;           // wide rows: bulk-copy ring depth (0 = register prefetch)
+    int stage_bytes = 0;
+    size_t smem = 0;          // dynamic shared memory of the persistent kernel
 };
 
 template <class T> SkPlan sk_plan(int n, int num_sms);

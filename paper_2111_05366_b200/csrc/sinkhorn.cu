@@ -83,6 +83,23 @@ __device__ __forceinline__ void lse_combine(T &m, T &s, T m2, T s2) {
 __device__ __forceinline__ double *fslot(const SkArgs &a, int s) { return (s & 1) ? a.f[1] : a.f[0]; }
 __device__ __forceinline__ double *gslot(const SkArgs &a, int s) { return (s & 1) ? a.g[1] : a.g[0]; }
 
+__device__ __forceinline__ void sk_stamp(const SkArgs &a, int k, int i) {
+    if (a.trace && k == a.trace_k && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[blockIdx.x * 16 + i] = t;
+    }
+}
+
+// stamp that waits for `dep` (diagnostics only)
+__device__ __forceinline__ void sk_stamp_v(const SkArgs &a, int k, int i, double dep) {
+    if (a.trace && k == a.trace_k && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "d"(dep));
+        a.trace[blockIdx.x * 16 + i] = t;
+    }
+}
+
 // ------------------------------------------------------------------ pass body
 // Row bands are cyclic over row groups (grp, grp + ngrp, ...), so a group owns
 // the same rows every pass.  With CL == 1 a group is one CTA that owns whole
@@ -102,16 +119,6 @@ __device__ __forceinline__ uint32_t dsmem_map(const void *p, uint32_t rank) {
     uint32_t r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
     return r;
-}
-__device__ __forceinline__ float ld_dsmem(uint32_t addr, float) {
-    float v;
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-    return v;
-}
-__device__ __forceinline__ double ld_dsmem(uint32_t addr, double) {
-    double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-    return v;
 }
 // Remote (DSMEM) store of a pair that signals the receiver's mbarrier on arrival.
 __device__ __forceinline__ void st_async_pair(uint32_t raddr, float a, float b, uint32_t rbar) {
@@ -155,9 +162,32 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <class T, int CH, int R, int CL, int NT>
+// Raw 16-byte loads of one band of R rows over this thread's chunks (zero outside).
+template <class T, int CH, int R, int NT>
+__device__ __forceinline__ void load_band_g(const SkArgs &a, const Slice &sl, int band, int nbands,
+                                            typename VecT<T>::V (&dst)[R][CH]) {
+    using V = typename VecT<T>::V;
+    constexpr int VW = VecT<T>::W;
+    const T *G = static_cast<const T *>(a.G);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int col = sl.c0 + ((int)threadIdx.x + NT * c) * VW;
+            const int row = band * R + r;
+            if (band < nbands && row < a.n && col < sl.c1)
+                dst[r][c] = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + col));
+            else
+                memset(&dst[r][c], 0, sizeof(V));
+        }
+}
+
+// RES: this CTA owns at most one band, held in registers (xres) for the whole
+// solve -- G never changes between sweeps, so nothing is reloaded.
+template <class T, int CH, int R, int CL, int NT, bool RES = false>
 __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
-                                          const Slice &sl, RowXch<T, R, CL> *xch, unsigned &xi) {
+                                          const Slice &sl, RowXch<T, R, CL> *xch, unsigned &xi,
+                                          typename VecT<T>::V (&xres)[R][CH]) {
     using V = typename VecT<T>::V;
     constexpr int VW = VecT<T>::W;
     constexpr int NW = NT / 32;
@@ -169,7 +199,6 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
     const double *gin = gslot(a, k + 1);  // g_{k-1}
     const double *fprev = fslot(a, k + 1);
     double *fout = fslot(a, k);
-    const T *G = static_cast<const T *>(a.G);
     const double ks = SkMath<T>::kScale;
     const T coef = (T)(coef_d * ks);
     const T gmax = (T)gmax_d;
@@ -181,20 +210,14 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
     // Raw 16-byte loads of one band; the next band is prefetched while the
     // current one is reduced, so the L2/HBM latency overlaps the row combine.
     V xv[R][CH];
-    auto load_band = [&](int band, V (&dst)[R][CH]) {
+    if constexpr (RES) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int c = 0; c < CH; ++c) {
-                const int col = c0 + (tid + NT * c) * VW;
-                const int row = band * R + r;
-                if (band < nbands && row < n && col < c1)
-                    dst[r][c] = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + col));
-                else
-                    memset(&dst[r][c], 0, sizeof(V));
-            }
-    };
-    load_band(sl.grp, xv);
+            for (int c = 0; c < CH; ++c) xv[r][c] = xres[r][c];
+    } else {
+        load_band_g<T, CH, R, NT>(a, sl, sl.grp, nbands, xv);
+    }
 
     T gl[CH][VW], acc[CH][VW];
 #pragma unroll
@@ -221,7 +244,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
 #pragma unroll
                 for (int e = 0; e < VW; ++e) x[r][c][e] = pv[e];
             }
-        load_band(band + sl.ngrp, xv);  // prefetch
+        if constexpr (!RES) load_band_g<T, CH, R, NT>(a, sl, band + sl.ngrp, nbands, xv);  // prefetch
         // f_{k-1} of row r0 + lane (warp 0 checks the deviation), fetched early
         double fprev_v = 0.0;
         if (writer && warp == 0 && lane < R && k >= 2 && r0 + lane < n) fprev_v = __ldcg(fprev + r0 + lane);
@@ -238,6 +261,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
                     m[r] = vmax(m[r], arg);
                 }
         }
+        sk_stamp_v(a, k, 8, (double)m[0]);
         // Warp max first (shuffle + max only), then exponentials against the warp
         // max and a plain sum butterfly: no SFU op on the shuffle chain.  Rows past
         // the end get m = -inf (skipped everywhere); exponentials use mx, which is
@@ -276,6 +300,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], off);
         }
+        sk_stamp_v(a, k, 9, (double)s[0]);
         // Per-warp pairs into a parity-double-buffered slot: one block barrier per
         // band; every warp then finishes all R rows itself (lane r <- row r) in
         // the same fixed order, so the results agree bit-for-bit across warps.
@@ -347,6 +372,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
             }
             ++xi;
         }
+        sk_stamp_v(a, k, 10, (double)Sb);
         double lse_l = 0.0;
         if (lane < R) {
             lse_l = (double)Mb + SkMath<T>::lgt(Sb);  // scaled units
@@ -360,9 +386,11 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
                 devmax = fmax(devmax, dev);
             }
         }
+        sk_stamp_v(a, k, 11, lse_l);
         double lse_r[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) lse_r[r] = __shfl_sync(0xffffffffu, lse_l, r);
+        sk_stamp_v(a, k, 12, lse_r[0]);
         if (!rowonly) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -391,6 +419,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
             }
         }
     }
+    sk_stamp_v(a, k, 14, (double)acc[0][0]);
     __shared__ double s_dev[NW];
     // rows are finished by lanes 0..R-1: reduce over the whole warp first
 #pragma unroll
@@ -404,6 +433,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         // max of non-negative doubles == max of their bit patterns: order-independent
         if (a.dslot) atomicMax(a.dslot + (k & 1), (unsigned long long)__double_as_longlong(d));
     }
+    sk_stamp(a, k, 13);
 }
 
 // Clustered wide rows (CL > 1, one row per band): the cross-CTA row exchange is
@@ -614,10 +644,261 @@ __device__ __forceinline__ void pass_body_lag(const SkArgs &a, int k, int max_sw
     }
 }
 
+// ------------------------------------------------------------------ TMA-staged wide rows
+// Wide rows (one row per band, CL >= 1) stream through a ring of S shared-memory
+// stages filled by 1-D bulk copies (cp.async.bulk, mbarrier complete_tx).  The
+// ring runs ahead D = S-2 bands and wraps across sweeps (a CTA owns the same rows
+// every sweep), so HBM requests stay in flight through the row reductions, the
+// cluster exchange and the grid barriers.  No register prefetch copy: a thread
+// holds only its chunk of the current band.  The exponentials of band j are
+// written back in place and re-read by the lagged finish of band j (iteration
+// j+1), so a stage is refilled only after the block barrier of iteration j+2.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct WideRing {
+    char *base;        // S stages of stage_bytes
+    uint64_t *full;    // S mbarriers
+    int S, stage_bytes;
+    int nrows;         // rows this CTA processes per sweep
+    uint32_t copy_bytes;
+    unsigned issued;   // bands issued (thread 0)
+    unsigned used;     // bands consumed (all threads)
+};
+
+template <class T>
+__device__ __forceinline__ void ring_issue(const SkArgs &a, const Slice &sl, WideRing &rg) {
+    const unsigned b = rg.issued++;
+    const int row = sl.grp + (int)(b % (unsigned)rg.nrows) * sl.ngrp;
+    const int s = (int)(b % (unsigned)rg.S);
+    const T *src = static_cast<const T *>(a.G) + (int64_t)row * a.ld + sl.c0;
+    xbar_arm(&rg.full[s], rg.copy_bytes);
+    bulk_g2s(rg.base + (size_t)s * rg.stage_bytes, src, rg.copy_bytes, &rg.full[s]);
+}
+
+template <class T, int CH, int CL, int NT>
+__device__ __forceinline__ void pass_body_tma(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
+                                              const Slice &sl, RowXch<T, 1, CL> *xch, unsigned &xi, WideRing &rg) {
+    using V = typename VecT<T>::V;
+    constexpr int VW = VecT<T>::W;
+    constexpr int NW = NT / 32;
+    __shared__ T s_m[2][NW], s_s[2][NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = a.n;
+    const bool pre = (k == 0);
+    const bool rowonly = (k == max_sweeps + 1);
+    const double *gin = gslot(a, k + 1);
+    const double *fprev = fslot(a, k + 1);
+    double *fout = fslot(a, k);
+    const double ks = SkMath<T>::kScale;
+    const T coef = (T)(coef_d * ks);
+    const T gmax = (T)gmax_d;
+    const int c0 = sl.c0, c1 = sl.c1;
+    const bool writer = (sl.rank == 0);
+    const int D = rg.S - 2;
+
+    T gl[CH][VW], acc[CH][VW];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+            const int col = c0 + (tid + NT * c) * VW + e;
+            const T gv = (!pre && col < c1) ? (T)(__ldcg(gin + col) * ks) : T(0);
+            gl[c][e] = col < c1 ? gv : neg_inf<T>();
+            acc[c][e] = T(0);
+        }
+    double devmax = 0.0;
+    T mx_p = T(0), Mp = neg_inf<T>(), Sp = T(0);
+    double fprev_p = 0.0;
+    int row_p = -1;
+    unsigned band_p = 0;
+
+    auto stage_of = [&](unsigned b) { return reinterpret_cast<V *>(rg.base + (size_t)(b % (unsigned)rg.S) * rg.stage_bytes); };
+
+    auto finish = [&](unsigned jp) {
+        double lse = 0.0;
+        if (lane == 0) {
+            T M = Mp, S = Sp;
+            if constexpr (CL > 1) {
+                const int xs = jp & 3;
+                xbar_wait(&xch->bar[xs], (jp >> 2) & 1);
+                T mq[CL], sq[CL];
+#pragma unroll
+                for (int q = 0; q < CL; ++q) {
+                    mq[q] = (q == sl.rank) ? Mp : xch->pair[xs][q][0][0];
+                    sq[q] = (q == sl.rank) ? Sp : xch->pair[xs][q][0][1];
+                }
+                M = neg_inf<T>();
+#pragma unroll
+                for (int q = 0; q < CL; ++q) M = mq[q] > M ? mq[q] : M;
+                S = T(0);
+#pragma unroll
+                for (int q = 0; q < CL; ++q)
+                    if (mq[q] != neg_inf<T>()) S += sq[q] * SkMath<T>::ex(mq[q] - M);
+            }
+            lse = (double)M + SkMath<T>::lgt(S);
+            if (writer && warp == 0 && row_p < n) {
+                const double fnew = -lse * (1.0 / SkMath<T>::kScale);
+                double dev = 0.0;
+                if (pre) dev = SkMath<T>::dev(-fnew);
+                else if (k >= 2) dev = SkMath<T>::dev(fprev_p - fnew);
+                if (!pre) __stcg(fout + row_p, fnew);
+                devmax = fmax(devmax, dev);
+            }
+        }
+        lse = __shfl_sync(0xffffffffu, lse, 0);
+        if (!rowonly && row_p < n) {
+            const double colf = pre ? 0.0 : -lse;
+            const T sc = SkMath<T>::ex((T)((double)mx_p + colf));
+            const V *st = stage_of(band_p);
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int col = c0 + (tid + NT * c) * VW;
+                if (col < c1) {
+                    const V yv = st[tid + NT * c];
+                    const T *py = reinterpret_cast<const T *>(&yv);
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) acc[c][e] += py[e] * sc;
+                }
+            }
+        }
+    };
+
+    int it = 0;
+    for (int row = sl.grp; row < n; row += sl.ngrp, ++it) {
+        const unsigned b = rg.used++;
+        double fpv = 0.0;
+        if (writer && warp == 0 && lane == 0 && k >= 2) fpv = __ldcg(fprev + row);
+        xbar_wait(&rg.full[b % (unsigned)rg.S], (b / (unsigned)rg.S) & 1);
+        V *st = stage_of(b);
+        T x[CH][VW];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int col = c0 + (tid + NT * c) * VW;
+            V xv;
+            if (col < c1) xv = st[tid + NT * c];
+            else memset(&xv, 0, sizeof(V));
+            const T *pv = reinterpret_cast<const T *>(&xv);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) x[c][e] = pv[e];
+        }
+        T m = neg_inf<T>();
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                const T arg = coef * (gmax - x[c][e]) + gl[c][e];  // E_ij + g_j (sinkhorn.py:125)
+                x[c][e] = arg;
+                m = vmax(m, arg);
+            }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const T m2 = __shfl_xor_sync(0xffffffffu, m, off);
+            m = m2 > m ? m2 : m;
+        }
+        const T mx = (m == neg_inf<T>()) ? T(0) : m;
+        T sp[VW];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) sp[e] = T(0);
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int col = c0 + (tid + NT * c) * VW;
+            V yv;
+            T *py = reinterpret_cast<T *>(&yv);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                const T y = SkMath<T>::ex(x[c][e] - mx);
+                py[e] = y;
+                sp[e] += y;
+            }
+            if (!rowonly && col < c1) st[tid + NT * c] = yv;  // re-read by finish(b)
+        }
+        T sum = T(0);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) sum += sp[e];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        const int par = it & 1;
+        if (lane == 0) { s_m[par][warp] = m; s_s[par][warp] = sum; }
+        fence_proxy_async_smem();  // this thread's stage accesses precede later bulk refills
+        __syncthreads();
+        // stage of band b-2 is free: every thread has passed finish(b-2)
+        if (tid == 0) ring_issue<T>(a, sl, rg);
+        T Mb, Sb;
+        {
+            const T mw = lane < NW ? s_m[par][lane] : neg_inf<T>();
+            T M = mw;
+#pragma unroll
+            for (int off = NW / 2; off > 0; off >>= 1) {
+                const T m2 = __shfl_xor_sync(0xffffffffu, M, off);
+                M = m2 > M ? m2 : M;
+            }
+            T S = (mw != neg_inf<T>()) ? s_s[par][lane] * SkMath<T>::ex(mw - M) : T(0);
+#pragma unroll
+            for (int off = NW / 2; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+            Mb = M;
+            Sb = S;
+        }
+        const unsigned j = xi;
+        if constexpr (CL > 1) {
+            if (warp == 0 && lane == 0) {
+                const int xs = j & 3;
+                xbar_arm(&xch->bar[xs], (uint32_t)((CL - 1) * 2 * sizeof(T)));
+#pragma unroll
+                for (int q = 0; q < CL; ++q)
+                    if (q != sl.rank)
+                        st_async_pair(dsmem_map(&xch->pair[xs][sl.rank][0][0], q), Mb, Sb, dsmem_map(&xch->bar[xs], q));
+            }
+        }
+        if (it > 0) finish(j - 1);
+        mx_p = mx;
+        Mp = Mb;
+        Sp = Sb;
+        fprev_p = fpv;
+        row_p = row;
+        band_p = b;
+        ++xi;
+        (void)D;
+    }
+    if (it > 0) finish(xi - 1);
+    if (!rowonly) {
+        T *cp = static_cast<T *>(a.colpart) + (int64_t)sl.grp * a.ldp;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int col = c0 + (tid + NT * c) * VW;
+            if (col < c1) {
+                V v;
+                T *pv = reinterpret_cast<T *>(&v);
+#pragma unroll
+                for (int e = 0; e < VW; ++e) pv[e] = acc[c][e];
+                __stcg(reinterpret_cast<V *>(cp + col), v);
+            }
+        }
+    }
+    __shared__ double s_dev[NW];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) devmax = fmax(devmax, __shfl_xor_sync(0xffffffffu, devmax, off));
+    if (lane == 0) s_dev[warp] = devmax;
+    __syncthreads();
+    if (tid == 0) {
+        double d = 0.0;
+        for (int w = 0; w < NW; ++w) d = fmax(d, s_dev[w]);
+        __stcg(a.devpart + blockIdx.x, d);
+        if (a.dslot) atomicMax(a.dslot + (k & 1), (unsigned long long)__double_as_longlong(d));
+    }
+}
+
 // Exact column LSE for a column whose partial sum under/overflowed:
 // g_j = -LSE_i(E_ij + f_i) over all rows (fp64).  Rare repair path.
 template <class T>
-__device__ double sk_exact_col(const SkArgs &a, int j, const double *f, bool pre, double coef, double gmax) {
+__device__ __noinline__ double sk_exact_col(const SkArgs &a, int j, const double *f, bool pre, double coef, double gmax) {
     const T *G = static_cast<const T *>(a.G);
     double M = -INFINITY;
     for (int i = 0; i < a.n; ++i) {
@@ -688,21 +969,6 @@ __device__ __forceinline__ void merge_body(const SkArgs &a, int k, double coef, 
     }
 }
 
-// Max of cnt per-CTA values: one warp reads (coalesced), result broadcast via smem.
-__device__ __forceinline__ double max_of(const double *p, int cnt) {
-    __shared__ double s_max;
-    if (threadIdx.x < 32) {
-        double d = 0.0;
-        for (int b = threadIdx.x; b < cnt; b += 32) d = fmax(d, __ldcg(p + b));
-        for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
-        if (threadIdx.x == 0) s_max = d;
-    }
-    __syncthreads();
-    const double d = s_max;
-    __syncthreads();
-    return d;
-}
-
 // Software grid barrier for a cooperative launch: arrival counter + generation.
 // Counter and generation live on different 128-byte lines so the spinning
 // readers do not contend with the arrivals.
@@ -727,7 +993,59 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks, un
 }
 
 // ------------------------------------------------------------------ drivers
-template <class T, int CH, int R, int CL, int NT>
+template <class T, int CH, int R, int CL, int NT, bool RES, bool TMA>
+__device__ __forceinline__ void sk_sweeps(const SkArgs &a, unsigned *bar, const Slice &sl, RowXch<T, R, CL> *xchp,
+                                          unsigned &xi, int k0, int K, double tol, double coef, double gmax,
+                                          typename VecT<T>::V (&xres)[R][CH], WideRing *rg) {
+    const int blk = blockIdx.x, nblk = gridDim.x;
+    unsigned epoch = 0;
+    for (int k = k0;; ++k) {
+        sk_stamp(a, k, 0);
+        if constexpr (TMA) pass_body_tma<T, CH, CL, NT>(a, k, K, coef, gmax, sl, xchp, xi, *rg);
+        else if constexpr (CL > 1 && R == 1) pass_body_lag<T, CH, CL, NT>(a, k, K, coef, gmax, sl, xchp, xi);
+        else pass_body<T, CH, R, CL, NT, RES>(a, k, K, coef, gmax, sl, xchp, xi, xres);
+        sk_stamp(a, k, 1);
+        grid_barrier(bar, nblk, epoch);
+        sk_stamp(a, k, 3);
+        const double drow = __longlong_as_double((long long)__ldcg(a.dslot + (k & 1)));
+        if (blk == 0 && threadIdx.x == 0) a.dslot[(k + 1) & 1] = 0ull;  // next sweep's slot
+        int stop = 0, sweeps = 0, conv = 0, slot = 0;
+        if (k >= 2) {
+            if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
+            else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
+        }
+        if (!stop) {
+            merge_body<T, NT>(a, k, coef, gmax, blk, nblk);
+            sk_stamp(a, k, 4);
+            grid_barrier(bar, nblk, epoch);
+            sk_stamp(a, k, 5);
+            if (k == 0) {
+                const double d0 = fmax(drow, __longlong_as_double((long long)__ldcg(a.dslot + 2)));
+                if (d0 < tol) { stop = 1; sweeps = 0; conv = 1; slot = 0; }
+                if (blk == 0 && threadIdx.x == 0) a.st->last_dev = d0;
+                if (stop && blk == 0 && threadIdx.x == 0) a.st->dev = d0;
+            }
+        } else if (blk == 0 && threadIdx.x == 0) {
+            a.st->dev = drow;
+        }
+        if (stop) {
+            if (blk == 0 && threadIdx.x == 0) {
+                a.st->done = 1; a.st->sweeps = sweeps; a.st->converged = conv; a.st->slot = slot;
+                a.st->k = k + 1;
+            }
+            if constexpr (TMA) {
+                // drain the bulk copies already issued for the next sweep
+                if (threadIdx.x == 0)
+                    for (unsigned b = rg->used; b < rg->issued; ++b)
+                        xbar_wait(&rg->full[b % (unsigned)rg->S], (b / (unsigned)rg->S) & 1);
+            }
+            if constexpr (CL > 1) cluster_sync();
+            return;
+        }
+    }
+}
+
+template <class T, int CH, int R, int CL, int NT, bool TMA = false>
 __global__ void __launch_bounds__(NT, (NT > 256 ? 1 : 2)) sk_persistent_kernel(SkArgs a, unsigned *bar) {
     __shared__ int s_k;
     if (threadIdx.x == 0) s_k = a.st->k;
@@ -757,39 +1075,39 @@ __global__ void __launch_bounds__(NT, (NT > 256 ? 1 : 2)) sk_persistent_kernel(S
         }
         cluster_sync();  // every peer's barriers exist before the first st.async
     }
-    unsigned epoch = 0;
-    for (int k = k0;; ++k) {
-        if constexpr (CL > 1 && R == 1) pass_body_lag<T, CH, CL, NT>(a, k, K, coef, gmax, sl, &xch, xi);
-        else pass_body<T, CH, R, CL, NT>(a, k, K, coef, gmax, sl, &xch, xi);
-        grid_barrier(bar, nblk, epoch);
-        const double drow = __longlong_as_double((long long)__ldcg(a.dslot + (k & 1)));
-        if (blk == 0 && threadIdx.x == 0) a.dslot[(k + 1) & 1] = 0ull;  // next sweep's slot
-        int stop = 0, sweeps = 0, conv = 0, slot = 0;
-        if (k >= 2) {
-            if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
-            else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
+    using V = typename VecT<T>::V;
+    V xres[R][CH];
+    if constexpr (TMA) {
+        static_assert(R == 1, "TMA ring streams one row per band");
+        extern __shared__ __align__(128) char sk_ring[];
+        __shared__ uint64_t full[8];
+        WideRing rg;
+        rg.base = sk_ring;
+        rg.full = full;
+        rg.S = a.stages;
+        rg.stage_bytes = a.stage_bytes;
+        rg.nrows = (a.n - sl.grp + sl.ngrp - 1) / sl.ngrp;
+        rg.copy_bytes = (uint32_t)(((sl.c1 - sl.c0 + VecT<T>::W - 1) / VecT<T>::W) * sizeof(V));
+        rg.issued = 0;
+        rg.used = 0;
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < rg.S; ++q) xbar_init(&full[q]);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            for (int q = 0; q < rg.S - 2; ++q) ring_issue<T>(a, sl, rg);
         }
-        if (!stop) {
-            merge_body<T, NT>(a, k, coef, gmax, blk, nblk);
-            grid_barrier(bar, nblk, epoch);
-            if (k == 0) {
-                const double d0 = fmax(drow, __longlong_as_double((long long)__ldcg(a.dslot + 2)));
-                if (d0 < tol) { stop = 1; sweeps = 0; conv = 1; slot = 0; }
-                if (blk == 0 && threadIdx.x == 0) a.st->last_dev = d0;
-                if (stop && blk == 0 && threadIdx.x == 0) a.st->dev = d0;
-            }
-        } else if (blk == 0 && threadIdx.x == 0) {
-            a.st->dev = drow;
-        }
-        if (stop) {
-            if (blk == 0 && threadIdx.x == 0) {
-                a.st->done = 1; a.st->sweeps = sweeps; a.st->converged = conv; a.st->slot = slot;
-                a.st->k = k + 1;
-            }
-            if constexpr (CL > 1) cluster_sync();
+        __syncthreads();
+        sk_sweeps<T, CH, R, CL, NT, false, true>(a, bar, sl, &xch, xi, k0, K, tol, coef, gmax, xres, &rg);
+        return;
+    }
+    if constexpr (CL == 1) {
+        const int nbands = (a.n + R - 1) / R;
+        if (a.resident && nbands <= nblk) {
+            load_band_g<T, CH, R, NT>(a, sl, sl.grp, nbands, xres);
+            sk_sweeps<T, CH, R, CL, NT, true, false>(a, bar, sl, &xch, xi, k0, K, tol, coef, gmax, xres, nullptr);
             return;
         }
     }
+    sk_sweeps<T, CH, R, CL, NT, false, false>(a, bar, sl, &xch, xi, k0, K, tol, coef, gmax, xres, nullptr);
 }
 
 template <class T, int CH, int R>
@@ -803,7 +1121,8 @@ __global__ void __launch_bounds__(kThreads, 2) sk_pass_kernel(SkArgs a) {
     if (s_done) return;
     const Slice sl{0, a.n, (int)blockIdx.x, (int)gridDim.x, 0};
     unsigned xi = 0;
-    pass_body<T, CH, R, 1, kThreads>(a, s_k, a.st->max_sweeps, a.st->coef, a.st->gmax, sl, nullptr, xi);
+    typename VecT<T>::V unused[R][CH];
+    pass_body<T, CH, R, 1, kThreads>(a, s_k, a.st->max_sweeps, a.st->coef, a.st->gmax, sl, nullptr, xi, unused);
 }
 
 template <class T>
@@ -911,11 +1230,11 @@ constexpr int rows_for(int ch) { return ch == 1 ? 8 : ch == 2 ? 4 : ch <= 4 ? 2 
 constexpr int kWideThreads = 512;
 constexpr int rows_for(int ch, int nt) { return nt == kThreads ? rows_for(ch) : 1; }
 
-template <class T, int CH, int CL, int NT> void *persistent_fn() {
-    return (void *)sk_persistent_kernel<T, CH, rows_for(CH, NT), CL, NT>;
+template <class T, int CH, int CL, int NT, bool TMA = false> void *persistent_fn() {
+    return (void *)sk_persistent_kernel<T, CH, rows_for(CH, NT), CL, NT, TMA>;
 }
 
-template <class T> void *persistent_for(int ch, int cl, int nt) {
+template <class T> void *persistent_for(int ch, int cl, int nt, bool tma = false) {
     if (nt == kThreads && cl == 1) {
         switch (ch) {
             case 1: return persistent_fn<T, 1, 1, kThreads>();
@@ -928,16 +1247,16 @@ template <class T> void *persistent_for(int ch, int cl, int nt) {
             case 8: return persistent_fn<T, 8, 1, kThreads>();
         }
     }
-#define GOAT_CL(C)                                                   \
-    if (nt == kWideThreads && cl == C) {                             \
-        switch (ch) {                                                \
-            case 3: return persistent_fn<T, 3, C, kWideThreads>();   \
-            case 4: return persistent_fn<T, 4, C, kWideThreads>();   \
-            case 5: return persistent_fn<T, 5, C, kWideThreads>();   \
-            case 6: return persistent_fn<T, 6, C, kWideThreads>();   \
-            case 7: return persistent_fn<T, 7, C, kWideThreads>();   \
-            case 8: return persistent_fn<T, 8, C, kWideThreads>();   \
-        }                                                            \
+#define GOAT_CL(C)                                                                                       \
+    if (nt == kWideThreads && cl == C) {                                                                 \
+        switch (ch) {                                                                                    \
+            case 3: return tma ? persistent_fn<T, 3, C, kWideThreads, true>() : persistent_fn<T, 3, C, kWideThreads>(); \
+            case 4: return tma ? persistent_fn<T, 4, C, kWideThreads, true>() : persistent_fn<T, 4, C, kWideThreads>(); \
+            case 5: return tma ? persistent_fn<T, 5, C, kWideThreads, true>() : persistent_fn<T, 5, C, kWideThreads>(); \
+            case 6: return tma ? persistent_fn<T, 6, C, kWideThreads, true>() : persistent_fn<T, 6, C, kWideThreads>(); \
+            case 7: return tma ? persistent_fn<T, 7, C, kWideThreads, true>() : persistent_fn<T, 7, C, kWideThreads>(); \
+            case 8: return tma ? persistent_fn<T, 8, C, kWideThreads, true>() : persistent_fn<T, 8, C, kWideThreads>(); \
+        }                                                                                                \
     }
     GOAT_CL(1)
     GOAT_CL(2)
@@ -957,18 +1276,19 @@ cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunch
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.nblk);
     cfg.blockDim = dim3(p.nt);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = p.smem;
     cfg.stream = s;
     attrs[0].id = cudaLaunchAttributeCooperative;
     // GOAT_SK_NOCOOP=1 drops the cooperative flag (profilers cannot replay it);
     // the grid is still sized to the co-resident maximum.
     attrs[0].val.cooperative = env_int("GOAT_SK_NOCOOP", 0) ? 0 : 1;
     attrs[1].id = cudaLaunchAttributeClusterDimension;
-    attrs[1].val.clusterDim.x = p.cl;
+    const int cdim = p.cl;
+    attrs[1].val.clusterDim.x = cdim;
     attrs[1].val.clusterDim.y = 1;
     attrs[1].val.clusterDim.z = 1;
     cfg.attrs = attrs;
-    cfg.numAttrs = p.cl > 1 ? 2 : 1;
+    cfg.numAttrs = cdim > 1 ? 2 : 1;
     return cfg;
 }
 
@@ -984,26 +1304,43 @@ template <class T> SkPlan sk_plan(int n, int num_sms) {
     p.nt = kThreads;
     p.slice_w = (int)round_up(n, 8 * VW);
     p.ch = ceil_div(ceil_div(n, VW), kThreads);
+    const int maxch = std::max(3, std::min(kMaxCh, env_int("GOAT_SK_MAXCH", kMaxCh)));
+    bool wide = false;
     if (p.ch > kMaxCh) {
-        // wide rows: 512-thread CTAs, then clusters of 2/4/8 splitting the row
+        // wide rows: 512-thread CTAs (or two 256-thread CTAs per SM), then
+        // clusters of 2/4/8 splitting the row
+        wide = true;
         p.nt = kWideThreads;
-        p.ch = std::max(3, ceil_div(ceil_div(n, VW), kWideThreads));
-        while (p.ch > kMaxCh && p.cl < 8) {
+        p.ch = std::max(3, ceil_div(ceil_div(n, VW), p.nt));
+        while (p.ch > maxch && p.cl < 8) {
             p.cl *= 2;
             p.slice_w = (int)round_up(ceil_div(n, p.cl), 8 * VW);
-            p.ch = std::max(3, ceil_div(ceil_div(p.slice_w, VW), kWideThreads));
+            p.ch = std::max(3, ceil_div(ceil_div(p.slice_w, VW), p.nt));
         }
     }
     if (p.ch > kMaxCh)
         throw Error(GOAT_ENOTSUP, "sinkhorn: order " + std::to_string(n) + " exceeds 8-CTA clusters of this build");
-    p.rows = rows_for(p.ch, p.nt);
+    p.rows = wide ? 1 : rows_for(p.ch, p.nt);
     const int nbands = (n + p.rows - 1) / p.rows;
+    // Cluster-split wide rows stream through the bulk-copy ring (measured: +30%
+    // at n = 20000-40000); unsplit wide rows keep the register prefetch, which
+    // measured faster at n = 10000 (profiles/round1_sk_tune.md).
+    if (wide && p.cl > 1 && env_int("GOAT_SK_TMA", 1)) {
+        // as many row-slice stages as ~200 KB of shared memory holds
+        p.stage_bytes = (int)round_up((size_t)p.slice_w * sizeof(T), 128);
+        p.stages = std::max(3, std::min(8, 200 * 1024 / p.stage_bytes));
+        if (const int st = env_int("GOAT_SK_STAGES", 0)) p.stages = std::max(3, std::min(8, st));
+        p.smem = (size_t)p.stages * p.stage_bytes;
+        GOAT_CUDA(cudaFuncSetAttribute(persistent_for<T>(p.ch, p.cl, p.nt, true),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    }
+    void *const kfn = persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
     p.persistent = env_int("GOAT_SK_PERSISTENT", 1) != 0 || p.nt != kThreads;
     // Co-resident groups (CTAs, or clusters of cl CTAs) for the cooperative launch.
     int groups = 0;
     if (p.cl == 1) {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)persistent_for<T>(p.ch, 1, p.nt), p.nt, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)kfn, p.nt, p.smem);
         groups = std::max(1, occ) * num_sms;  // measured: all co-resident CTAs is fastest (n <= 5000)
     } else {
         cudaLaunchAttribute attrs[2];
@@ -1015,7 +1352,7 @@ template <class T> SkPlan sk_plan(int n, int num_sms) {
         cfg.attrs = &cattr;
         cfg.numAttrs = 1;
         int ncl = 0;
-        GOAT_CUDA(cudaOccupancyMaxActiveClusters(&ncl, persistent_for<T>(p.ch, p.cl, p.nt), &cfg));
+        GOAT_CUDA(cudaOccupancyMaxActiveClusters(&ncl, kfn, &cfg));
         groups = std::max(1, ncl);
     }
     int ngrp = std::max(1, std::min(nbands, groups));
@@ -1062,10 +1399,14 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
     args.dslot = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(bar) + 512);
     args.nblk = p.ngrp;  // column-partial rows = row groups
     args.slice_w = p.slice_w;
+    args.resident = env_int("GOAT_SK_RES", 1);
+    args.stages = p.stages;
+    args.stage_bytes = p.stage_bytes;
     void *params[] = {&args, &bar};
     cudaLaunchAttribute attrs[2];
     cudaLaunchConfig_t cfg = persistent_config(p, s, attrs);
-    GOAT_CUDA(cudaLaunchKernelExC(&cfg, persistent_for<T>(p.ch, p.cl, p.nt), params));
+    void *fn = persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
+    GOAT_CUDA(cudaLaunchKernelExC(&cfg, fn, params));
     note_launch();
 }
 
