@@ -178,7 +178,7 @@ def run_ours(args):
     h = _lib.handle(local, "fp32")
     lib = _lib.load()
     stream = torch.cuda.current_stream(dev)
-    _lib.check(lib.goat_set_stream(h.ptr, ctypes_ptr(stream.cuda_stream)))
+    _lib.check(lib.goat_set_stream(h.ptr, _lib.stream_handle(stream)))
 
     dA = torch.from_numpy(A.astype(np.float32)).to(dev)
     dB = torch.from_numpy(B.astype(np.float32)).to(dev)
@@ -308,11 +308,6 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def ctypes_ptr(x):
-    import ctypes
-    return ctypes.c_void_p(int(x))
 
 
 def _ms_per_sweep(lib, h, n, G, reps=200):

@@ -158,6 +158,58 @@ int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int3
 int goat_bench_gradient(goat_handle *h, int64_t n, const void *dA, const void *dB, const void *dX,
                         int32_t reps, double *ms, int32_t *products, int32_t *terms);
 
+/* lap.py:48-58 on a device matrix (handle precision, leading dim ldm); the
+ * final projection of the row-sharded driver after it gathers G. */
+int goat_lap_device(goat_handle *h, int64_t n, const void *dM, int64_t ldm, int32_t sense,
+                    int64_t *assignment, double *objective, int32_t *certified);
+
+/* ---- Row-sharded primitives (one process per GPU) ----------
+ * The reference has no distributed path; these split _fw_core's per-iteration
+ * work (matcher.py:177-212) by row blocks.  A rank owns rows [r0, r0+m) of the
+ * n x n iterates P, Q, G; every block buffer is m x ld and full matrices are
+ * n x ld with ld = round_up(n, 8) (device, handle precision).  The caller runs
+ * the collectives between the calls (paper_2111_05366_b200/sharded.py: NCCL
+ * through torch.distributed):
+ *   gradient      all-gather Q -> goat_shard_gradient
+ *   Sinkhorn      per sweep: goat_shard_lot_pass -> all-gather the (n+1)-vector
+ *                 -> goat_shard_lot_merge (identical on every rank)
+ *   line search   goat_shard_dots -> sum-allreduce of 6 doubles
+ *   final LAP     all-gather G -> goat_lap_device.
+ * dAT_rows = NULL declares A and B symmetric (G = 2 A Q B). */
+int goat_shard_setup(goat_handle *h, int64_t n, int64_t m, const void *dA_rows, const void *dAT_rows,
+                     const void *dB, int64_t ld);
+/* G_r = (A_r Q) B^T + (A^T_r Q) B from the gathered Q (n x ld). */
+int goat_shard_gradient(goat_handle *h, const void *dQ_full, void *dOut_rows);
+/* local (min, max) of a block (the LOT scale is global: min/max-allreduce). */
+int goat_shard_minmax(goat_handle *h, const void *dX_rows, double *out2);
+/* sinkhorn.py:103-130 set-up from the GLOBAL min/max of the cost. */
+int goat_shard_lot_begin(goat_handle *h, int32_t sense, double lam, double gmin, double gmax,
+                         int32_t max_sweeps, double tol);
+/* one pass over the block: dSend[0..n) = fp64 column sums, dSend[n] = max row deviation.
+ * No-op once the loop has stopped. */
+int goat_shard_lot_pass(goat_handle *h, const void *dG_rows, double *dSend);
+/* merge the gathered dRecv[world][n+1] in rank order: stopping rule + new column potentials.
+ * A column sum that under/overflows leaves the sweep pending (passes and merges
+ * are no-ops) until the repair round below has run. */
+int goat_shard_lot_merge(goat_handle *h, const double *dRecv, int32_t world);
+/* repair round: exact fp64 (max, sumexp) pairs of the flagged columns over the
+ * block -> dPairs[2n]; all-gather; rank-order combine that finishes the sweep
+ * (the multi-GPU form of the single-GPU exact column LSE). */
+int goat_shard_lot_repair_pass(goat_handle *h, const void *dG_rows, double *dPairs);
+int goat_shard_lot_repair_merge(goat_handle *h, const double *dRecvPairs, int32_t world);
+/* loop state (synchronises): done, sweeps, converged, deviation, columns repaired so far,
+ * repair round pending. */
+int goat_shard_lot_status(goat_handle *h, int32_t *done, int32_t *sweeps, int32_t *converged,
+                          double *deviation, int32_t *repaired, int32_t *pending);
+/* Q_r = exp(E + f + g) of the returned iterate (1/n when the cost was constant). */
+int goat_shard_lot_emit(goat_handle *h, const void *dG_rows, void *dQ_rows);
+/* local line-search sums of goat_fw_core's dots: <GQ,D>, <GP-GQ,D>, <GQ,Q>, |D|^2, 0, 0 (D = P - Q). */
+int goat_shard_dots(goat_handle *h, const void *GP, const void *GQ, const void *P, const void *Q,
+                    double *out6);
+/* Y = a X + b Y on a block (matcher.py:197); fill a block with a constant (core.py:89-93). */
+int goat_shard_axpby(goat_handle *h, double a, const void *dX_rows, double b, void *dY_rows);
+int goat_shard_fill(goat_handle *h, double value, void *dX_rows);
+
 /* Library build/feature string, e.g. "goat sm_100a tcgen05". */
 const char *goat_version(void);
 

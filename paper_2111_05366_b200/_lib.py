@@ -94,6 +94,26 @@ def _bind(lib):
         "goat_bench_gradient": (ctypes.c_int, [H, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                                ctypes.c_void_p, ctypes.c_int32, _c_double_p, _c_i32_p,
                                                _c_i32_p]),
+        "goat_lap_device": (ctypes.c_int, [H, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                           _c_i64_p, _c_double_p, _c_i32_p]),
+        "goat_shard_setup": (ctypes.c_int, [H, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_int64]),
+        "goat_shard_gradient": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_void_p]),
+        "goat_shard_minmax": (ctypes.c_int, [H, ctypes.c_void_p, _c_double_p]),
+        "goat_shard_lot_begin": (ctypes.c_int, [H, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                                ctypes.c_double, ctypes.c_int32, ctypes.c_double]),
+        "goat_shard_lot_pass": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_void_p]),
+        "goat_shard_lot_merge": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_int32]),
+        "goat_shard_lot_status": (ctypes.c_int, [H, _c_i32_p, _c_i32_p, _c_i32_p, _c_double_p, _c_i32_p,
+                                                 _c_i32_p]),
+        "goat_shard_lot_repair_pass": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_void_p]),
+        "goat_shard_lot_repair_merge": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_int32]),
+        "goat_shard_lot_emit": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_void_p]),
+        "goat_shard_dots": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, _c_double_p]),
+        "goat_shard_axpby": (ctypes.c_int, [H, ctypes.c_double, ctypes.c_void_p, ctypes.c_double,
+                                            ctypes.c_void_p]),
+        "goat_shard_fill": (ctypes.c_int, [H, ctypes.c_double, ctypes.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -107,7 +127,11 @@ EXPORTS = ("goat_create", "goat_destroy", "goat_last_error", "goat_version", "go
            "goat_fw_core", "goat_fw_core_device", "goat_gradient", "goat_lot",
            "goat_sinkhorn_knopp", "goat_line_search_coeffs", "goat_lap",
            "goat_qap_objective_perm", "goat_set_stream", "goat_bench_sweep",
-           "goat_bench_gradient")
+           "goat_bench_gradient", "goat_lap_device", "goat_shard_setup", "goat_shard_gradient",
+           "goat_shard_minmax", "goat_shard_lot_begin", "goat_shard_lot_pass", "goat_shard_lot_merge",
+           "goat_shard_lot_status", "goat_shard_lot_repair_pass", "goat_shard_lot_repair_merge",
+           "goat_shard_lot_emit", "goat_shard_dots", "goat_shard_axpby",
+           "goat_shard_fill")
 
 
 def load():
@@ -177,6 +201,14 @@ def handle(device=0, precision="fp64", gemm="auto") -> Handle:
             h = Handle(device, precision, gemm)
             _handles[key] = h
         return h
+
+
+def stream_handle(torch_stream) -> ctypes.c_void_p:
+    """cudaStream_t for goat_set_stream from a torch.cuda.Stream.  torch's default
+    stream has handle 0, which goat_set_stream reads as "the handle's own stream";
+    map it to cudaStreamLegacy (0x1) so the library really shares torch's stream."""
+    s = int(torch_stream.cuda_stream)
+    return ctypes.c_void_p(s if s != 0 else 1)
 
 
 def dptr(a: np.ndarray):

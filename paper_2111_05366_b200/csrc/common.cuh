@@ -70,7 +70,7 @@ struct SkState {
     int slot;       // potentials slot holding the returned (f, g)
     int arrive;     // last-block-done counter for the merge kernel
     int repaired;   // columns recomputed by the exact LSE repair (diagnostic)
-    int pad;
+    int pending;    // row-sharded driver: a column repair round is due before sweep k can finish
     double dev;     // returned deviation
     double last_dev;
     // per-LOT parameters (device-resident so a captured sweep graph is reusable)
@@ -79,6 +79,7 @@ struct SkState {
     double tol;
     int max_sweeps;
     int log_mode;
+    double dcol;    // row-sharded pre-check: column deviation of the columns that needed no repair
 };
 
 // Count of kernels this library launched (reported as gpu_launches).

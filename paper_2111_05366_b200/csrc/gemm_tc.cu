@@ -319,8 +319,8 @@ __global__ void split_planes_t_kernel(const float *X, int64_t ldx, int n, __nv_b
 }
 
 // 1 if every entry is exactly representable in bf16 (so one plane is exact).
-__global__ void bf16_exact_kernel(const float *X, int64_t ldx, int n, int *flag) {
-    for (int i = blockIdx.x; i < n; i += gridDim.x)
+__global__ void bf16_exact_kernel(const float *X, int64_t ldx, int n, int rows, int *flag) {
+    for (int i = blockIdx.x; i < rows; i += gridDim.x)
         for (int j = threadIdx.x; j < n; j += blockDim.x) {
             const float v = X[(int64_t)i * ldx + j];
             if (__bfloat162float(__float2bfloat16_rn(v)) != v) *flag = 0;
@@ -398,10 +398,11 @@ void tc_split_planes_t(const float *X, int64_t ldx, int n, __nv_bfloat16 *planes
     GOAT_CHECK_LAUNCH();
 }
 
-bool tc_bf16_exact(const float *X, int64_t ldx, int n, int *dflag, cudaStream_t s) {
+bool tc_bf16_exact(const float *X, int64_t ldx, int n, int *dflag, cudaStream_t s, int rows) {
     const int one = 1;
+    if (rows < 0) rows = n;
     GOAT_CUDA(cudaMemcpyAsync(dflag, &one, sizeof(int), cudaMemcpyHostToDevice, s));
-    bf16_exact_kernel<<<std::min(n, 2048), 256, 0, s>>>(X, ldx, n, dflag);
+    bf16_exact_kernel<<<std::max(1, std::min(rows, 2048)), 256, 0, s>>>(X, ldx, n, rows, dflag);
     note_launch();
     int r = 0;
     GOAT_CUDA(cudaMemcpyAsync(&r, dflag, sizeof(int), cudaMemcpyDeviceToHost, s));

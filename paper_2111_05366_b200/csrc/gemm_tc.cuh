@@ -54,6 +54,6 @@ void tc_split_planes(const float *X, int64_t ldx, int rows, int cols, __nv_bfloa
                      int64_t plane_stride, int nplanes, cudaStream_t s);
 void tc_split_planes_t(const float *X, int64_t ldx, int n, __nv_bfloat16 *planes, int64_t ldp, int64_t plane_stride,
                        int nplanes, cudaStream_t s);
-bool tc_bf16_exact(const float *X, int64_t ldx, int n, int *dflag, cudaStream_t s);
+bool tc_bf16_exact(const float *X, int64_t ldx, int n, int *dflag, cudaStream_t s, int rows = -1);
 
 }  // namespace goat

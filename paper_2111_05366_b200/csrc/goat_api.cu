@@ -48,6 +48,16 @@ struct Handle {
     // the iterate X and the intermediate Y^T.
     DevBuf tcA, tcAt, tcB, tcX, tcY, tcS;
     int tc_na = 0, tc_nb = 0;  // planes of A / B (1 when exact in bf16)
+    // row-sharded primitives (goat_shard_*): this rank's block of rows
+    struct Shard {
+        int64_t n = 0, m = 0;
+        bool sym = false, tc = false, ready = false, fill = false;
+        DevBuf A, AT, B, X;       // A rows, A^T rows (m x ld), B (n x ld), GEMM intermediate
+        DevBuf pA, pB, pQT, pX;   // tcgen05 planes: [A_r; A^T_r], [B; B^T], Q^T, [X; X2]
+        int na = 0, nb = 0;
+        SkPlan plan;
+        DevBuf bad;               // per-column repair flags of the current sweep
+    } sh;
     double *h_scal = nullptr;                   // pinned host scalars
     int lap_stats[4] = {0, 0, 0, 0};            // last auction: assigned, rounds, capped, freed
     SkState *h_state = nullptr;                 // pinned
@@ -158,6 +168,48 @@ void tc_prepare(Ctx &c, const float *A, const float *B) {
     }
 }
 
+// Split-K: the tensor core's fp32 accumulation error grows with the number of
+// chained MMAs; accuracy comes from in-kernel promotion (chunk k-steps per TMEM
+// chain), and split-K slices (reduced in fixed order) only fill the SMs when
+// there are few output tiles.
+void tc_set_slices(const Handle &h, TcGemmParams &g, int rows, int cols, int64_t ld, int kblocks) {
+    const int steps = g.nterms * kblocks;
+    const int tiles = ceil_div(cols, tc_block_n()) * ceil_div(rows, tc_block_m());
+    int sl = std::min(8, ceil_div(2 * h.num_sms, tiles));
+    if (const char *e = getenv("GOAT_TC_KSLICES")) sl = std::max(1, atoi(e));
+    const int64_t cap = (int64_t)1 << 31;
+    while (sl > 1 && (int64_t)sl * rows * ld * 4 > cap) --sl;
+    sl = std::max(1, std::min(sl, steps));
+    g.kpb = ceil_div(steps, sl);
+    g.kslices = ceil_div(steps, g.kpb);
+    const char *ce = getenv("GOAT_TC_CHUNK");
+    g.chunk = ce ? std::max(1, atoi(ce)) : 4;  // measured: 2-6e-7 of max|G|, speed flat in chunk
+}
+
+// Run a prepared product: mode-1 output (bf16 planes) or fp32 C = alpha * sum of terms,
+// through split-K slices when set_slices chose them.
+void tc_run(Handle &h, TcGemmParams &g, int rows, int cols, int64_t ld, float alpha, float *C,
+            __nv_bfloat16 *planes, int64_t plane_stride, int nplanes, cudaStream_t s) {
+    const int64_t out_stride = (int64_t)rows * ld;
+    if (g.kslices == 1) {
+        g.alpha = alpha;
+        if (planes) {
+            g.mode = 1; g.planes = planes; g.ldpl = ld; g.plane_stride = plane_stride; g.nplanes = nplanes;
+            g.C = nullptr; g.ldc = 0; g.slice_stride = 0;
+        } else {
+            g.mode = 0; g.C = C; g.ldc = ld; g.slice_stride = 0; g.planes = nullptr; g.nplanes = 0;
+        }
+        tc_gemm(g, s);
+        return;
+    }
+    h.tcS.ensure((size_t)g.kslices * out_stride * 4);
+    g.mode = 0; g.alpha = 1.f; g.C = h.tcS.as<float>(); g.ldc = ld; g.slice_stride = out_stride;
+    g.planes = nullptr; g.nplanes = 0;
+    tc_gemm(g, s);
+    tc_slice_reduce(h.tcS.as<float>(), out_stride, g.kslices, rows, cols, ld, alpha, planes ? nullptr : C, planes,
+                    plane_stride, planes ? nplanes : 0, s);
+}
+
 // out = A X B^T + A^T X B on tensor cores:
 //   Y^T = [B; B^T] X^T   (M = n or 2n)        -> bf16 planes of Y^T
 //   G   = A Y1 + A^T Y2  (K-concatenated)     -> fp32
@@ -171,24 +223,7 @@ void tc_gradient(Ctx &c, const float *X, float *out) {
     tc_split_planes(X, ld, n, n, px, ld, mat, S, c.s);
     const int64_t ystride = (int64_t)yrows * ld;
     const int kblocks = ceil_div(n, tc_block_k());
-    // Split-K: the tensor core's fp32 accumulation error grows with the number of
-    // chained MMAs, so the K range is cut into slices reduced in fixed order with
-    // round-to-nearest adds; slices also fill the SMs when there are few tiles.
-    // Accuracy comes from in-kernel promotion (chunk k-steps per TMEM chain);
-    // split-K slices only fill the SMs when there are few output tiles.
-    auto set_slices = [&](TcGemmParams &g, int rows) {
-        const int steps = g.nterms * kblocks;
-        const int tiles = ceil_div(n, tc_block_n()) * ceil_div(rows, tc_block_m());
-        int sl = std::min(8, ceil_div(2 * h.num_sms, tiles));
-        if (const char *e = getenv("GOAT_TC_KSLICES")) sl = std::max(1, atoi(e));
-        const int64_t cap = (int64_t)1 << 31;
-        while (sl > 1 && (int64_t)sl * rows * ld * 4 > cap) --sl;
-        sl = std::max(1, std::min(sl, steps));
-        g.kpb = ceil_div(steps, sl);
-        g.kslices = ceil_div(steps, g.kpb);
-        const char *ce = getenv("GOAT_TC_CHUNK");
-        g.chunk = ce ? std::max(1, atoi(ce)) : 4;  // measured: 2-6e-7 of max|G|, speed flat in chunk
-    };
+    auto set_slices = [&](TcGemmParams &g, int rows) { tc_set_slices(h, g, rows, n, ld, kblocks); };
     static thread_local TcGemmParams g1, g2;
     // Y^T = [B; B^T] X^T
     g1.nterms = 0;
@@ -666,6 +701,106 @@ template <class F> void dispatch(Handle &h, F &&f) {
     else f((double *)nullptr);
 }
 
+// ------------------------------------------------------------------ row-sharded primitives
+// One rank owns rows [r0, r0 + m) of the n x n iterates (the caller's row block;
+// every block buffer is m x ld, ld = ld_for(n)).  The gradient of a block is
+//     G_r = (A_r Q) B^T + (A^T_r Q) B          (symmetric: 2 (A_r Q) B)
+// which needs the whole Q (the caller all-gathers it) and B, both replicated;
+// A_r and A^T_r are the block's rows of A and A^T.  Both chains are two
+// row-local products of m x n x n, so the work divides by the rank count.
+__global__ void assign_sum_kernel(const float *Mf, const double *Md, int64_t ld, const int *perm, int n,
+                                  double *out) {
+    __shared__ double s_r[32];
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        v += Mf ? (double)Mf[(int64_t)i * ld + perm[i]] : Md[(int64_t)i * ld + perm[i]];
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) s_r[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_r[w];
+        *out = t;
+    }
+}
+
+void shard_tc_prepare(Handle &h) {
+    auto &S = h.sh;
+    const int n = (int)S.n, m = (int)S.m;
+    const int64_t ld = ld_for(n), mat = (int64_t)n * ld;
+    cudaStream_t s = h.stream;
+    int *flag = h.ivec.as<int>();
+    const float *A = S.A.as<float>(), *AT = S.AT.as<float>(), *B = S.B.as<float>();
+    const bool a_exact = tc_bf16_exact(A, ld, n, flag, s, m) && (S.sym || tc_bf16_exact(AT, ld, n, flag, s, m));
+    S.na = a_exact ? 1 : h.split;
+    S.nb = tc_bf16_exact(B, ld, n, flag, s) ? 1 : h.split;
+    const int arows = S.sym ? m : 2 * m, brows = S.sym ? n : 2 * n;
+    const int64_t astride = (int64_t)arows * ld, bstride = (int64_t)brows * ld;
+    S.pA.ensure((size_t)astride * 2 * S.na);
+    S.pB.ensure((size_t)bstride * 2 * S.nb);
+    S.pQT.ensure((size_t)mat * 2 * h.split);
+    S.pX.ensure((size_t)astride * 2 * h.split);
+    auto *pa = S.pA.as<__nv_bfloat16>();
+    auto *pb = S.pB.as<__nv_bfloat16>();
+    tc_split_planes(A, ld, m, n, pa, ld, astride, S.na, s);
+    if (!S.sym) tc_split_planes(AT, ld, m, n, pa + (int64_t)m * ld, ld, astride, S.na, s);
+    tc_split_planes(B, ld, n, n, pb, ld, bstride, S.nb, s);
+    if (!S.sym) tc_split_planes_t(B, ld, n, pb + mat, ld, bstride, S.nb, s);
+}
+
+template <class T> void shard_gradient(Handle &h, const T *Q, T *out) {
+    auto &S = h.sh;
+    const int n = (int)S.n, m = (int)S.m;
+    const int64_t ld = ld_for(n), mat = (int64_t)n * ld;
+    cudaStream_t s = h.stream;
+    if constexpr (std::is_same<T, float>::value) {
+        if (S.tc) {
+            const int SP = h.split;
+            const int arows = S.sym ? m : 2 * m, brows = S.sym ? n : 2 * n;
+            const int64_t astride = (int64_t)arows * ld, bstride = (int64_t)brows * ld;
+            const int kblocks = ceil_div(n, tc_block_k());
+            auto *pqt = S.pQT.as<__nv_bfloat16>();
+            auto *px = S.pX.as<__nv_bfloat16>();
+            tc_split_planes_t(Q, ld, n, pqt, ld, mat, SP, s);  // K-major operand of A_r Q
+            static thread_local TcGemmParams g1, g2;
+            // [X; X2] = [A_r; A^T_r] Q   -> bf16 planes
+            g1.nterms = 0;
+            add_terms(g1, S.pA.as<__nv_bfloat16>(), S.na, astride, arows, 0, pqt, SP, mat, n, 0, ld, n);
+            g1.M = arows; g1.N = n; g1.K = n; g1.kblocks = kblocks;
+            tc_set_slices(h, g1, arows, n, ld, kblocks);
+            tc_run(h, g1, arows, n, ld, 1.f, nullptr, px, astride, SP, s);
+            // G_r = X B^T + X2 B   (symmetric: 2 X B)
+            g2.nterms = 0;
+            add_terms(g2, px, SP, astride, arows, 0, S.pB.as<__nv_bfloat16>(), S.nb, bstride, brows, 0, ld, n);
+            if (!S.sym) add_terms(g2, px, SP, astride, arows, m, S.pB.as<__nv_bfloat16>(), S.nb, bstride, brows, n, ld, n);
+            g2.M = m; g2.N = n; g2.K = n; g2.kblocks = kblocks;
+            tc_set_slices(h, g2, m, n, ld, kblocks);
+            tc_run(h, g2, m, n, ld, S.sym ? 2.f : 1.f, out, nullptr, 0, 0, s);
+            return;
+        }
+    }
+    T *X = S.X.as<T>();
+    const T *A = S.A.as<T>(), *AT = S.AT.as<T>(), *B = S.B.as<T>();
+    gemm_simt<T>(m, n, n, 1.0, A, ld, 0, Q, ld, 0, 0.0, X, ld, s);                          // A_r Q
+    gemm_simt<T>(m, n, n, S.sym ? 2.0 : 1.0, X, ld, 0, B, ld, S.sym ? 0 : 1, 0.0, out, ld, s);  // (A_r Q) B^T
+    if (!S.sym) {
+        gemm_simt<T>(m, n, n, 1.0, AT, ld, 0, Q, ld, 0, 0.0, X, ld, s);   // A^T_r Q
+        gemm_simt<T>(m, n, n, 1.0, X, ld, 0, B, ld, 0, 1.0, out, ld, s);  // + (A^T_r Q) B
+    }
+}
+
+template <class T> SkArgs shard_sk_args(Handle &h, const void *G) {
+    auto &S = h.sh;
+    SkArgs a{};
+    a.G = G; a.ld = ld_for(S.n); a.n = (int)S.n; a.m = (int)S.m;
+    a.f[0] = h.f[0].as<double>(); a.f[1] = h.f[1].as<double>();
+    a.g[0] = h.g[0].as<double>(); a.g[1] = h.g[1].as<double>();
+    a.colpart = h.colpart.p; a.ldp = ld_for(S.n);
+    a.devpart = h.devpart.as<double>(); a.devcol = h.devcol.as<double>();
+    a.st = h.state.as<SkState>(); a.nblk = S.plan.nblk;
+    return a;
+}
+
 }  // namespace
 }  // namespace goat
 
@@ -1045,6 +1180,260 @@ int goat_qap_objective_perm(goat_handle *h, int64_t n, const double *A, int64_t 
         GOAT_CUDA(cudaMemcpyAsync(h->h_scal + 40, h->scal.as<double>() + 40, 8, cudaMemcpyDeviceToHost, c.s));
         sync(c);
         *objective = h->h_scal[40];
+    });
+}
+
+
+// ------------------------------------------------------------------ row-sharded C ABI
+static goat::Handle::Shard &shard_of(goat_handle *h) {
+    require(h && h->sh.ready, "goat_shard_setup has not been called on this handle");
+    return h->sh;
+}
+
+int goat_shard_setup(goat_handle *h, int64_t n, int64_t m, const void *dA_rows, const void *dAT_rows,
+                     const void *dB, int64_t ld) {
+    return guarded([&] {
+        require(h && dA_rows && dB, "NULL argument");
+        check_order(n);
+        require(m >= 1 && m <= n, "block rows must be in [1, n]");
+        require(ld >= n, "leading dimension < n");
+        ensure_workspace(*h, n);
+        auto &S = h->sh;
+        S.ready = false;
+        S.n = n; S.m = m; S.sym = (dAT_rows == nullptr); S.fill = false;
+        const int64_t lw = ld_for(n);
+        const size_t es = h->precision == GOAT_FP32 ? 4 : 8;
+        cudaStream_t s = h->stream;
+        auto put = [&](DevBuf &dst, const void *src, int64_t rows) {
+            dst.ensure((size_t)rows * lw * es);
+            GOAT_CUDA(cudaMemsetAsync(dst.p, 0, (size_t)rows * lw * es, s));
+            GOAT_CUDA(cudaMemcpy2DAsync(dst.p, lw * es, src, ld * es, n * es, rows, cudaMemcpyDeviceToDevice, s));
+        };
+        put(S.A, dA_rows, m);
+        if (!S.sym) put(S.AT, dAT_rows, m);
+        put(S.B, dB, n);
+        S.X.ensure((size_t)m * lw * es);
+        S.tc = h->precision == GOAT_FP32 && h->gemm != GOAT_GEMM_SIMT;
+        if (S.tc) shard_tc_prepare(*h);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            S.plan = sk_plan<T>((int)n, h->num_sms, (int)m);
+        });
+        h->colpart.ensure(S.plan.colpart_bytes);
+        S.bad.ensure((size_t)ld_for(n));
+        GOAT_CUDA(cudaStreamSynchronize(s));
+        S.ready = true;
+    });
+}
+
+int goat_shard_gradient(goat_handle *h, const void *dQ_full, void *dOut_rows) {
+    return guarded([&] {
+        shard_of(h);
+        require(dQ_full && dOut_rows, "NULL argument");
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            shard_gradient<T>(*h, static_cast<const T *>(dQ_full), static_cast<T *>(dOut_rows));
+        });
+        GOAT_CHECK_LAUNCH();
+    });
+}
+
+int goat_shard_minmax(goat_handle *h, const void *dX_rows, double *out2) {
+    return guarded([&] {
+        auto &S = shard_of(h);
+        require(dX_rows && out2, "NULL argument");
+        double *mm = h->scal.as<double>();
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            launch_minmax<T>(static_cast<const T *>(dX_rows), ld_for(S.n), (int)S.n, h->red.as<double>(), mm,
+                             h->stream, (int)S.m);
+        });
+        GOAT_CUDA(cudaMemcpyAsync(h->h_scal, mm, 16, cudaMemcpyDeviceToHost, h->stream));
+        GOAT_CUDA(cudaStreamSynchronize(h->stream));
+        out2[0] = h->h_scal[0];
+        out2[1] = h->h_scal[1];
+    });
+}
+
+int goat_shard_lot_begin(goat_handle *h, int32_t sense, double lam, double gmin, double gmax, int32_t max_sweeps,
+                         double tol) {
+    return guarded([&] {
+        auto &S = shard_of(h);
+        require(sense == GOAT_MINIMIZE || sense == GOAT_MAXIMIZE, "bad objective sense");
+        require(lam > 0 && tol > 0 && max_sweeps >= 1, "bad Sinkhorn parameters");
+        const double scale = gmax - gmin;  // sinkhorn.py:115-119, global over all ranks
+        SkState st0{};
+        S.fill = (scale == 0.0);           // sinkhorn.py:121-124: exact barycenter
+        if (S.fill) {
+            st0.done = 1; st0.sweeps = 0; st0.converged = 1; st0.dev = 0.0;
+        } else {
+            const bool maximize = (sense == GOAT_MAXIMIZE);
+            st0.gmax = maximize ? gmax : gmin;
+            st0.coef = maximize ? -lam / scale : lam / scale;
+            st0.log_mode = !(std::exp((-lam / scale) * scale) > 0.0);
+            st0.k = st0.log_mode ? 1 : 0;
+            st0.tol = tol;
+            st0.max_sweeps = max_sweeps;
+        }
+        const int64_t lw = ld_for(S.n);
+        GOAT_CUDA(cudaMemsetAsync(h->f[0].p, 0, lw * 8, h->stream));
+        GOAT_CUDA(cudaMemsetAsync(h->g[0].p, 0, lw * 8, h->stream));
+        *h->h_state = st0;
+        GOAT_CUDA(cudaMemcpyAsync(h->state.p, h->h_state, sizeof(SkState), cudaMemcpyHostToDevice, h->stream));
+    });
+}
+
+int goat_shard_lot_pass(goat_handle *h, const void *dG_rows, double *dSend) {
+    return guarded([&] {
+        auto &S = shard_of(h);
+        require(dG_rows && dSend, "NULL argument");
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            SkArgs a = shard_sk_args<T>(*h, dG_rows);
+            sk_launch_shard_pass<T>(a, S.plan, h->bar.as<unsigned>(), dSend, h->stream);
+        });
+    });
+}
+
+int goat_shard_lot_merge(goat_handle *h, const double *dRecv, int32_t world) {
+    return guarded([&] {
+        shard_of(h);
+        require(dRecv && world >= 1, "bad argument");
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            SkArgs a = shard_sk_args<T>(*h, nullptr);
+            sk_launch_shard_merge<T>(a, dRecv, world, h->sh.bad.as<unsigned char>(), h->stream);
+        });
+    });
+}
+
+int goat_shard_lot_repair_pass(goat_handle *h, const void *dG_rows, double *dPairs) {
+    return guarded([&] {
+        shard_of(h);
+        require(dG_rows && dPairs, "NULL argument");
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            SkArgs a = shard_sk_args<T>(*h, dG_rows);
+            sk_launch_shard_repair_pass<T>(a, h->sh.bad.as<unsigned char>(), dPairs, h->stream);
+        });
+    });
+}
+
+int goat_shard_lot_repair_merge(goat_handle *h, const double *dRecvPairs, int32_t world) {
+    return guarded([&] {
+        shard_of(h);
+        require(dRecvPairs && world >= 1, "bad argument");
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            SkArgs a = shard_sk_args<T>(*h, nullptr);
+            sk_launch_shard_repair_merge(a, dRecvPairs, world, h->sh.bad.as<unsigned char>(), h->stream);
+        });
+    });
+}
+
+int goat_shard_lot_status(goat_handle *h, int32_t *done, int32_t *sweeps, int32_t *converged, double *deviation,
+                          int32_t *repaired, int32_t *pending) {
+    return guarded([&] {
+        shard_of(h);
+        GOAT_CUDA(cudaMemcpyAsync(h->h_state, h->state.p, sizeof(SkState), cudaMemcpyDeviceToHost, h->stream));
+        GOAT_CUDA(cudaStreamSynchronize(h->stream));
+        const SkState &st = *h->h_state;
+        if (done) *done = st.done;
+        if (sweeps) *sweeps = st.sweeps;
+        if (converged) *converged = st.converged;
+        if (deviation) *deviation = st.dev;
+        if (repaired) *repaired = st.repaired;
+        if (pending) *pending = st.pending;
+    });
+}
+
+int goat_shard_lot_emit(goat_handle *h, const void *dG_rows, void *dQ_rows) {
+    return guarded([&] {
+        auto &S = shard_of(h);
+        require(dG_rows && dQ_rows, "NULL argument");
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            if (S.fill) {
+                launch_fill<T>(static_cast<T *>(dQ_rows), ld_for(S.n), (int)S.n, 1.0 / (double)S.n, h->stream, (int)S.m);
+            } else {
+                SkArgs a = shard_sk_args<T>(*h, dG_rows);
+                sk_launch_emit<T>(a, static_cast<T *>(dQ_rows), ld_for(S.n), nullptr, 0, nullptr, 0,
+                                  h->red.as<double>(), kRedBlocks, h->stream);
+            }
+        });
+    });
+}
+
+int goat_shard_dots(goat_handle *h, const void *GP, const void *GQ, const void *P, const void *Q, double *out6) {
+    return guarded([&] {
+        auto &S = shard_of(h);
+        require(GP && GQ && P && Q && out6, "NULL argument");
+        double *dots = h->scal.as<double>() + 16;
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            launch_fw_dots<T>(static_cast<const T *>(GP), static_cast<const T *>(GQ), static_cast<const T *>(P),
+                              static_cast<const T *>(Q), nullptr, ld_for(S.n), (int)S.n, h->red.as<double>(), dots,
+                              h->stream, (int)S.m);
+        });
+        GOAT_CUDA(cudaMemcpyAsync(h->h_scal + 16, dots, 6 * 8, cudaMemcpyDeviceToHost, h->stream));
+        GOAT_CUDA(cudaStreamSynchronize(h->stream));
+        for (int q = 0; q < 6; ++q) out6[q] = h->h_scal[16 + q];
+    });
+}
+
+int goat_shard_axpby(goat_handle *h, double a, const void *dX_rows, double b, void *dY_rows) {
+    return guarded([&] {
+        auto &S = shard_of(h);
+        require(dX_rows && dY_rows, "NULL argument");
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            launch_axpby<T>(a, static_cast<const T *>(dX_rows), b, static_cast<T *>(dY_rows), ld_for(S.n), (int)S.n,
+                            h->stream, (int)S.m);
+        });
+    });
+}
+
+int goat_shard_fill(goat_handle *h, double value, void *dX_rows) {
+    return guarded([&] {
+        auto &S = shard_of(h);
+        require(dX_rows, "NULL argument");
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            launch_fill<T>(static_cast<T *>(dX_rows), ld_for(S.n), (int)S.n, value, h->stream, (int)S.m);
+        });
+    });
+}
+
+int goat_lap_device(goat_handle *h, int64_t n, const void *dM, int64_t ldm, int32_t sense, int64_t *assignment,
+                    double *objective, int32_t *certified) {
+    return guarded([&] {
+        require(h && dM && assignment, "NULL argument");
+        check_order(n);
+        require(ldm >= n, "leading dimension < n");
+        require(sense == GOAT_MINIMIZE || sense == GOAT_MAXIMIZE, "sense must be minimize or maximize");
+        ensure_workspace(*h, n);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            Ctx c(*h, (int)n);
+            const size_t es = sizeof(T);
+            GOAT_CUDA(cudaMemsetAsync(h->M.p, 0, (size_t)n * c.ld * es, c.s));
+            GOAT_CUDA(cudaMemcpy2DAsync(h->M.p, c.ld * es, dM, ldm * es, n * es, n, cudaMemcpyDeviceToDevice, c.s));
+            std::vector<int> ph;
+            const int cert = run_lap<T>(c, h->M.as<T>(), sense, h->ivec.as<int>(), ph);
+            if (certified) *certified = cert;
+            for (int64_t r = 0; r < n; ++r) assignment[r] = ph[r];
+            if (objective) {
+                double *o = h->scal.as<double>() + 56;
+                const bool f32 = std::is_same<T, float>::value;
+                assign_sum_kernel<<<1, 1024, 0, c.s>>>(f32 ? (const float *)h->M.p : nullptr,
+                                                       f32 ? nullptr : (const double *)h->M.p, c.ld,
+                                                       h->ivec.as<int>(), (int)n, o);
+                note_launch();
+                GOAT_CUDA(cudaMemcpyAsync(h->h_scal + 56, o, 8, cudaMemcpyDeviceToHost, c.s));
+                sync(c);
+                *objective = h->h_scal[56];
+            }
+        });
     });
 }
 

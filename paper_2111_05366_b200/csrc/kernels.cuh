@@ -11,7 +11,9 @@ namespace goat {
 struct SkArgs {
     const void *G;      // n x n, element type = precision, leading dim ld
     int64_t ld;
-    int n;
+    int n;              // columns (and rows unless m > 0)
+    int m = 0;          // rows of a row-sharded block (0 = n)
+    int single_pass = 0;  // row-sharded driver: run pass st->k only, then exit
     double *f[2];       // row potentials, ring of 2 (fp64)
     double *g[2];       // column potentials, ring of 2 (fp64)
     void *colpart;      // [nblk][ldp] per-CTA column partial sums (element type)
@@ -45,13 +47,31 @@ struct SkPlan {
     size_t smem = 0;          // dynamic shared memory of the persistent kernel
 };
 
-template <class T> SkPlan sk_plan(int n, int num_sms);
+// rows: rows of a row-sharded block (-1 = n).
+template <class T> SkPlan sk_plan(int n, int num_sms, int rows = -1);
 template <class T> void sk_launch_pass(const SkArgs &a, const SkPlan &p, cudaStream_t s);
 template <class T> void sk_launch_merge(const SkArgs &a, const SkPlan &p, cudaStream_t s);
 // All sweeps in one cooperative launch (bar: 2 unsigned of scratch).
 template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, unsigned *bar, cudaStream_t s);
 // Q = exp(E + f + g) for the returned slot; optional fused partial sums:
 // part[blk*4 + 0] = sum (Q-P)^2, [1] = <L,Q>.  P, L may be null.
+// Row-sharded sweep (one rank's rows; the caller all-gathers `send` between):
+//   sk_launch_shard_pass: pass st->k over the block (no-op once done), then
+//     send[0..n) = fp64 column sums of the block, send[n] = its max row deviation;
+//   sk_launch_shard_merge: fixed-order merge of recv[world][n+1], the stopping rule
+//     and g_k (identical on every rank).
+template <class T> void sk_launch_shard_pass(const SkArgs &a, const SkPlan &p, unsigned *bar, double *send,
+                                             cudaStream_t s);
+template <class T>
+void sk_launch_shard_merge(const SkArgs &a, const double *recv, int world, unsigned char *bad, cudaStream_t s);
+//   column repair round (only when the merge left the sweep pending):
+//   sk_launch_shard_repair_pass: exact fp64 (max, sumexp) pairs of the flagged
+//     columns over the block's rows -> pair[2n]; the caller all-gathers them;
+//   sk_launch_shard_repair_merge: rank-order combine, finishes the sweep.
+template <class T>
+void sk_launch_shard_repair_pass(const SkArgs &a, const unsigned char *bad, double *pair, cudaStream_t s);
+void sk_launch_shard_repair_merge(const SkArgs &a, const double *recv, int world, const unsigned char *bad,
+                                  cudaStream_t s);
 template <class T>
 void sk_launch_emit(const SkArgs &a, T *Q, int64_t ldq, const T *P, int64_t ldp, const T *L,
                     int64_t ldl, double *part, int nblk, cudaStream_t s);
@@ -60,11 +80,11 @@ void sk_launch_emit(const SkArgs &a, T *Q, int64_t ldq, const T *P, int64_t ldp,
 // Deterministic two-stage reductions (fixed grid, fixed order).
 constexpr int kRedBlocks = 296;
 template <class T>
-void launch_minmax(const T *X, int64_t ld, int n, double *part, double *out2, cudaStream_t s);
+void launch_minmax(const T *X, int64_t ld, int n, double *part, double *out2, cudaStream_t s, int rows = -1);
 // D = P - Q: out[0]=<GQ,D>, [1]=<GP-GQ,D>, [2]=<GQ,Q>, [3]=|D|^2, [4]=<L,D>, [5]=<L,Q>
 template <class T>
 void launch_fw_dots(const T *GP, const T *GQ, const T *P, const T *Q, const T *L, int64_t ld, int n,
-                    double *part, double *out6, cudaStream_t s);
+                    double *part, double *out6, cudaStream_t s, int rows = -1);
 // out[0] = sum_ij A_ij * B_{p(i)p(j)}  (A, B fp64)
 void launch_qap_perm(const double *A, int64_t lda, const double *B, int64_t ldb,
                      const int *perm, int n, double *part, double *out, cudaStream_t s);
@@ -74,15 +94,15 @@ void launch_convert(const double *src, int64_t lds, T *dst, int64_t ldd, int n, 
 template <class T>
 void launch_convert_to_f64(const T *src, int64_t lds, double *dst, int64_t ldd, int n,
                            cudaStream_t s);
-template <class T> void launch_fill(T *dst, int64_t ld, int n, double value, cudaStream_t s);
+template <class T> void launch_fill(T *dst, int64_t ld, int n, double value, cudaStream_t s, int rows = -1);
 // Y = a*X + b*Y  (elementwise, matcher.py:197)
 template <class T>
-void launch_axpby(double a, const T *X, double b, T *Y, int64_t ld, int n, cudaStream_t s);
+void launch_axpby(double a, const T *X, double b, T *Y, int64_t ld, int n, cudaStream_t s, int rows = -1);
 // Q = permutation matrix of perm (core.py:64-70)
 template <class T> void launch_perm_matrix(const int *perm, T *Q, int64_t ld, int n, cudaStream_t s);
 // Y = X + L
 template <class T>
-void launch_add(const T *X, const T *L, T *Y, int64_t ld, int n, cudaStream_t s);
+void launch_add(const T *X, const T *L, T *Y, int64_t ld, int n, cudaStream_t s, int rows = -1);
 // G_ij = (ra_i rb_j + ca_i cb_j) / n  (gradient at the barycenter, rank 2)
 template <class T>
 void launch_bary_grad(const T *A, int64_t lda, const T *B, int64_t ldb, T *G, int64_t ldg,

@@ -45,10 +45,10 @@ __global__ void finish_sum_kernel(const double *part, int nb, double *out) {
 }
 
 template <class T>
-__global__ void minmax_kernel(const T *X, int64_t ld, int n, double *part) {
+__global__ void minmax_kernel(const T *X, int64_t ld, int n, int rows, double *part) {
     __shared__ double smin[kThreads / 32], smax[kThreads / 32];
     double lo = INFINITY, hi = -INFINITY;
-    for (int i = blockIdx.x; i < n; i += gridDim.x)
+    for (int i = blockIdx.x; i < rows; i += gridDim.x)
         for (int j = threadIdx.x; j < n; j += kThreads) {
             double x = (double)X[(int64_t)i * ld + j];
             lo = fmin(lo, x);
@@ -80,9 +80,9 @@ __global__ void minmax_finish_kernel(const double *part, int nb, double *out) {
 //   [0] <GQ, D>   [1] <GP - GQ, D>   [2] <GQ, Q>   [3] |D|^2   [4] <L, D>   [5] <L, Q>
 template <class T>
 __global__ void fw_dots_kernel(const T *GP, const T *GQ, const T *P, const T *Q, const T *L, int64_t ld,
-                               int n, double *part) {
+                               int n, int rows, double *part) {
     double v[6] = {0, 0, 0, 0, 0, 0};
-    for (int i = blockIdx.x; i < n; i += gridDim.x)
+    for (int i = blockIdx.x; i < rows; i += gridDim.x)
         for (int j = threadIdx.x; j < n; j += kThreads) {
             const int64_t o = (int64_t)i * ld + j;
             const double gq = GQ[o], gp = GP[o], q = Q[o];
@@ -127,14 +127,14 @@ __global__ void convert_to_f64_kernel(const T *src, int64_t lds, double *dst, in
 }
 
 template <class T>
-__global__ void fill_kernel(T *dst, int64_t ld, int n, T value) {
-    for (int i = blockIdx.x; i < n; i += gridDim.x)
+__global__ void fill_kernel(T *dst, int64_t ld, int n, int rows, T value) {
+    for (int i = blockIdx.x; i < rows; i += gridDim.x)
         for (int j = threadIdx.x; j < ld; j += kThreads) dst[(int64_t)i * ld + j] = (j < n) ? value : T(0);
 }
 
 template <class T>
-__global__ void axpby_kernel(T a, const T *X, T b, T *Y, int64_t ld, int n) {
-    for (int i = blockIdx.x; i < n; i += gridDim.x)
+__global__ void axpby_kernel(T a, const T *X, T b, T *Y, int64_t ld, int n, int rows) {
+    for (int i = blockIdx.x; i < rows; i += gridDim.x)
         for (int j = threadIdx.x; j < n; j += kThreads) {
             const int64_t o = (int64_t)i * ld + j;
             Y[o] = a * X[o] + b * Y[o];
@@ -150,8 +150,8 @@ __global__ void perm_matrix_kernel(const int *perm, T *Q, int64_t ld, int n) {
 }
 
 template <class T>
-__global__ void add_kernel(const T *X, const T *L, T *Y, int64_t ld, int n) {
-    for (int i = blockIdx.x; i < n; i += gridDim.x)
+__global__ void add_kernel(const T *X, const T *L, T *Y, int64_t ld, int n, int rows) {
+    for (int i = blockIdx.x; i < rows; i += gridDim.x)
         for (int j = threadIdx.x; j < n; j += kThreads) {
             const int64_t o = (int64_t)i * ld + j;
             Y[o] = X[o] + L[o];
@@ -213,16 +213,16 @@ __global__ void neglog_kernel(const T *X, int64_t ldx, T *Y, int64_t ldy, int n,
 }  // namespace
 
 template <class T>
-void launch_minmax(const T *X, int64_t ld, int n, double *part, double *out2, cudaStream_t s) {
-    minmax_kernel<T><<<kRedBlocks, kThreads, 0, s>>>(X, ld, n, part); note_launch();
+void launch_minmax(const T *X, int64_t ld, int n, double *part, double *out2, cudaStream_t s, int rows) {
+    minmax_kernel<T><<<kRedBlocks, kThreads, 0, s>>>(X, ld, n, rows < 0 ? n : rows, part); note_launch();
     minmax_finish_kernel<<<1, 32, 0, s>>>(part, kRedBlocks, out2); note_launch();
     GOAT_CHECK_LAUNCH();
 }
 
 template <class T>
 void launch_fw_dots(const T *GP, const T *GQ, const T *P, const T *Q, const T *L, int64_t ld, int n,
-                    double *part, double *out6, cudaStream_t s) {
-    fw_dots_kernel<T><<<kRedBlocks, kThreads, 0, s>>>(GP, GQ, P, Q, L, ld, n, part); note_launch();
+                    double *part, double *out6, cudaStream_t s, int rows) {
+    fw_dots_kernel<T><<<kRedBlocks, kThreads, 0, s>>>(GP, GQ, P, Q, L, ld, n, rows < 0 ? n : rows, part); note_launch();
     finish_sum_kernel<6><<<1, kThreads, 0, s>>>(part, kRedBlocks, out6); note_launch();
     GOAT_CHECK_LAUNCH();
 }
@@ -247,14 +247,16 @@ void launch_convert_to_f64(const T *src, int64_t lds, double *dst, int64_t ldd, 
     GOAT_CHECK_LAUNCH();
 }
 
-template <class T> void launch_fill(T *dst, int64_t ld, int n, double value, cudaStream_t s) {
-    fill_kernel<T><<<std::min(n, 4096), kThreads, 0, s>>>(dst, ld, n, (T)value); note_launch();
+template <class T> void launch_fill(T *dst, int64_t ld, int n, double value, cudaStream_t s, int rows) {
+    if (rows < 0) rows = n;
+    fill_kernel<T><<<std::max(1, std::min(rows, 4096)), kThreads, 0, s>>>(dst, ld, n, rows, (T)value); note_launch();
     GOAT_CHECK_LAUNCH();
 }
 
 template <class T>
-void launch_axpby(double a, const T *X, double b, T *Y, int64_t ld, int n, cudaStream_t s) {
-    axpby_kernel<T><<<std::min(n, 4096), kThreads, 0, s>>>((T)a, X, (T)b, Y, ld, n); note_launch();
+void launch_axpby(double a, const T *X, double b, T *Y, int64_t ld, int n, cudaStream_t s, int rows) {
+    if (rows < 0) rows = n;
+    axpby_kernel<T><<<std::max(1, std::min(rows, 4096)), kThreads, 0, s>>>((T)a, X, (T)b, Y, ld, n, rows); note_launch();
     GOAT_CHECK_LAUNCH();
 }
 
@@ -263,8 +265,9 @@ template <class T> void launch_perm_matrix(const int *perm, T *Q, int64_t ld, in
     GOAT_CHECK_LAUNCH();
 }
 
-template <class T> void launch_add(const T *X, const T *L, T *Y, int64_t ld, int n, cudaStream_t s) {
-    add_kernel<T><<<std::min(n, 4096), kThreads, 0, s>>>(X, L, Y, ld, n); note_launch();
+template <class T> void launch_add(const T *X, const T *L, T *Y, int64_t ld, int n, cudaStream_t s, int rows) {
+    if (rows < 0) rows = n;
+    add_kernel<T><<<std::max(1, std::min(rows, 4096)), kThreads, 0, s>>>(X, L, Y, ld, n, rows); note_launch();
     GOAT_CHECK_LAUNCH();
 }
 
@@ -291,15 +294,15 @@ void launch_neglog(const T *X, int64_t ldx, T *Y, int64_t ldy, int n, int *bad, 
 }
 
 #define GOAT_INST(T)                                                                                \
-    template void launch_minmax<T>(const T *, int64_t, int, double *, double *, cudaStream_t);        \
+    template void launch_minmax<T>(const T *, int64_t, int, double *, double *, cudaStream_t, int);   \
     template void launch_fw_dots<T>(const T *, const T *, const T *, const T *, const T *, int64_t, int, \
-                                    double *, double *, cudaStream_t);                               \
+                                    double *, double *, cudaStream_t, int);                          \
     template void launch_convert<T>(const double *, int64_t, T *, int64_t, int, double, cudaStream_t); \
     template void launch_convert_to_f64<T>(const T *, int64_t, double *, int64_t, int, cudaStream_t); \
-    template void launch_fill<T>(T *, int64_t, int, double, cudaStream_t);                           \
-    template void launch_axpby<T>(double, const T *, double, T *, int64_t, int, cudaStream_t);       \
+    template void launch_fill<T>(T *, int64_t, int, double, cudaStream_t, int);                      \
+    template void launch_axpby<T>(double, const T *, double, T *, int64_t, int, cudaStream_t, int);  \
     template void launch_perm_matrix<T>(const int *, T *, int64_t, int, cudaStream_t);               \
-    template void launch_add<T>(const T *, const T *, T *, int64_t, int, cudaStream_t);              \
+    template void launch_add<T>(const T *, const T *, T *, int64_t, int, cudaStream_t, int);         \
     template void launch_bary_grad<T>(const T *, int64_t, const T *, int64_t, T *, int64_t, int,     \
                                       double *, cudaStream_t);                                       \
     template void launch_is_symmetric<T>(const T *, int64_t, int, int *, cudaStream_t);              \

@@ -79,6 +79,9 @@ __device__ __forceinline__ void lse_combine(T &m, T &s, T m2, T s2) {
     s = a + b;
 }
 
+// Rows of this (possibly row-sharded) block; columns are always a.n.
+__device__ __forceinline__ int rows_of(const SkArgs &a) { return a.m > 0 ? a.m : a.n; }
+
 // Ring slots are selected, not indexed, so SkArgs stays in the parameter bank.
 __device__ __forceinline__ double *fslot(const SkArgs &a, int s) { return (s & 1) ? a.f[1] : a.f[0]; }
 __device__ __forceinline__ double *gslot(const SkArgs &a, int s) { return (s & 1) ? a.g[1] : a.g[0]; }
@@ -175,7 +178,7 @@ __device__ __forceinline__ void load_band_g(const SkArgs &a, const Slice &sl, in
         for (int c = 0; c < CH; ++c) {
             const int col = sl.c0 + ((int)threadIdx.x + NT * c) * VW;
             const int row = band * R + r;
-            if (band < nbands && row < a.n && col < sl.c1)
+            if (band < nbands && row < rows_of(a) && col < sl.c1)
                 dst[r][c] = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + col));
             else
                 memset(&dst[r][c], 0, sizeof(V));
@@ -206,7 +209,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
     const bool writer = (sl.rank == 0);  // one CTA per group writes f / deviation
 
     double devmax = 0.0;
-    const int nbands = (n + R - 1) / R;
+    const int nbands = (rows_of(a) + R - 1) / R;
     // Raw 16-byte loads of one band; the next band is prefetched while the
     // current one is reduced, so the L2/HBM latency overlaps the row combine.
     V xv[R][CH];
@@ -247,7 +250,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         if constexpr (!RES) load_band_g<T, CH, R, NT>(a, sl, band + sl.ngrp, nbands, xv);  // prefetch
         // f_{k-1} of row r0 + lane (warp 0 checks the deviation), fetched early
         double fprev_v = 0.0;
-        if (writer && warp == 0 && lane < R && k >= 2 && r0 + lane < n) fprev_v = __ldcg(fprev + r0 + lane);
+        if (writer && warp == 0 && lane < R && k >= 2 && r0 + lane < rows_of(a)) fprev_v = __ldcg(fprev + r0 + lane);
         T m[R], s[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -377,7 +380,7 @@ __device__ __forceinline__ void pass_body(const SkArgs &a, int k, int max_sweeps
         if (lane < R) {
             lse_l = (double)Mb + SkMath<T>::lgt(Sb);  // scaled units
             const int row = r0 + lane;
-            if (writer && warp == 0 && row < n) {
+            if (writer && warp == 0 && row < rows_of(a)) {
                 const double fnew = -lse_l * (1.0 / SkMath<T>::kScale);
                 double dev = 0.0;
                 if (pre) dev = SkMath<T>::dev(-fnew);                  // |rowsum(K) - 1|
@@ -450,7 +453,6 @@ __device__ __forceinline__ void pass_body_lag(const SkArgs &a, int k, int max_sw
     constexpr int NW = NT / 32;
     __shared__ T s_m[2][NW], s_s[2][NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n = a.n;
     const bool pre = (k == 0);
     const bool rowonly = (k == max_sweeps + 1);
     const double *gin = gslot(a, k + 1);
@@ -462,14 +464,14 @@ __device__ __forceinline__ void pass_body_lag(const SkArgs &a, int k, int max_sw
     const T gmax = (T)gmax_d;
     const int c0 = sl.c0, c1 = sl.c1;
     const bool writer = (sl.rank == 0);
-    const int nbands = n;
+    const int nbands = rows_of(a);
 
     V xv[CH];
     auto load_row = [&](int row, V (&dst)[CH]) {
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
             const int col = c0 + (tid + NT * c) * VW;
-            if (row < n && col < c1)
+            if (row < nbands && col < c1)
                 dst[c] = __ldg(reinterpret_cast<const V *>(G + (int64_t)row * a.ld + col));
             else
                 memset(&dst[c], 0, sizeof(V));
@@ -512,7 +514,7 @@ __device__ __forceinline__ void pass_body_lag(const SkArgs &a, int k, int max_sw
             for (int q = 0; q < CL; ++q)
                 if (mq[q] != neg_inf<T>()) S += sq[q] * SkMath<T>::ex(mq[q] - M);
             lse = (double)M + SkMath<T>::lgt(S);
-            if (writer && warp == 0 && row_p < n) {
+            if (writer && warp == 0 && row_p < nbands) {
                 const double fnew = -lse * (1.0 / SkMath<T>::kScale);
                 double dev = 0.0;
                 if (pre) dev = SkMath<T>::dev(-fnew);
@@ -522,7 +524,7 @@ __device__ __forceinline__ void pass_body_lag(const SkArgs &a, int k, int max_sw
             }
         }
         lse = __shfl_sync(0xffffffffu, lse, 0);
-        if (!rowonly && row_p < n) {
+        if (!rowonly && row_p < nbands) {
             const double colf = pre ? 0.0 : -lse;
             const T sc = SkMath<T>::ex((T)((double)mx_p + colf));
 #pragma unroll
@@ -675,6 +677,7 @@ struct WideRing {
 
 template <class T>
 __device__ __forceinline__ void ring_issue(const SkArgs &a, const Slice &sl, WideRing &rg) {
+    if (a.single_pass && rg.issued >= (unsigned)rg.nrows) return;  // one sweep per launch
     const unsigned b = rg.issued++;
     const int row = sl.grp + (int)(b % (unsigned)rg.nrows) * sl.ngrp;
     const int s = (int)(b % (unsigned)rg.S);
@@ -691,7 +694,6 @@ __device__ __forceinline__ void pass_body_tma(const SkArgs &a, int k, int max_sw
     constexpr int NW = NT / 32;
     __shared__ T s_m[2][NW], s_s[2][NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n = a.n;
     const bool pre = (k == 0);
     const bool rowonly = (k == max_sweeps + 1);
     const double *gin = gslot(a, k + 1);
@@ -744,7 +746,7 @@ __device__ __forceinline__ void pass_body_tma(const SkArgs &a, int k, int max_sw
                     if (mq[q] != neg_inf<T>()) S += sq[q] * SkMath<T>::ex(mq[q] - M);
             }
             lse = (double)M + SkMath<T>::lgt(S);
-            if (writer && warp == 0 && row_p < n) {
+            if (writer && warp == 0 && row_p < rows_of(a)) {
                 const double fnew = -lse * (1.0 / SkMath<T>::kScale);
                 double dev = 0.0;
                 if (pre) dev = SkMath<T>::dev(-fnew);
@@ -754,7 +756,7 @@ __device__ __forceinline__ void pass_body_tma(const SkArgs &a, int k, int max_sw
             }
         }
         lse = __shfl_sync(0xffffffffu, lse, 0);
-        if (!rowonly && row_p < n) {
+        if (!rowonly && row_p < rows_of(a)) {
             const double colf = pre ? 0.0 : -lse;
             const T sc = SkMath<T>::ex((T)((double)mx_p + colf));
             const V *st = stage_of(band_p);
@@ -772,7 +774,7 @@ __device__ __forceinline__ void pass_body_tma(const SkArgs &a, int k, int max_sw
     };
 
     int it = 0;
-    for (int row = sl.grp; row < n; row += sl.ngrp, ++it) {
+    for (int row = sl.grp; row < rows_of(a); row += sl.ngrp, ++it) {
         const unsigned b = rg.used++;
         double fpv = 0.0;
         if (writer && warp == 0 && lane == 0 && k >= 2) fpv = __ldcg(fprev + row);
@@ -1005,6 +1007,15 @@ __device__ __forceinline__ void sk_sweeps(const SkArgs &a, unsigned *bar, const 
         else if constexpr (CL > 1 && R == 1) pass_body_lag<T, CH, CL, NT>(a, k, K, coef, gmax, sl, xchp, xi);
         else pass_body<T, CH, R, CL, NT, RES>(a, k, K, coef, gmax, sl, xchp, xi, xres);
         sk_stamp(a, k, 1);
+        if (a.single_pass) {  // row-sharded driver: the caller reduces across ranks
+            if constexpr (TMA) {
+                if (threadIdx.x == 0)
+                    for (unsigned b = rg->used; b < rg->issued; ++b)
+                        xbar_wait(&rg->full[b % (unsigned)rg->S], (b / (unsigned)rg->S) & 1);
+            }
+            if constexpr (CL > 1) cluster_sync();
+            return;
+        }
         grid_barrier(bar, nblk, epoch);
         sk_stamp(a, k, 3);
         const double drow = __longlong_as_double((long long)__ldcg(a.dslot + (k & 1)));
@@ -1047,9 +1058,10 @@ __device__ __forceinline__ void sk_sweeps(const SkArgs &a, unsigned *bar, const 
 
 template <class T, int CH, int R, int CL, int NT, bool TMA = false>
 __global__ void __launch_bounds__(NT, (NT > 256 ? 1 : 2)) sk_persistent_kernel(SkArgs a, unsigned *bar) {
-    __shared__ int s_k;
-    if (threadIdx.x == 0) s_k = a.st->k;
+    __shared__ int s_k, s_done;
+    if (threadIdx.x == 0) { s_k = a.st->k; s_done = a.st->done | a.st->pending; }
     __syncthreads();
+    if (a.single_pass && s_done) return;  // every CTA sees the same flags
     const int k0 = s_k;
     const int K = a.st->max_sweeps;
     const double tol = a.st->tol, coef = a.st->coef, gmax = a.st->gmax;
@@ -1086,7 +1098,7 @@ __global__ void __launch_bounds__(NT, (NT > 256 ? 1 : 2)) sk_persistent_kernel(S
         rg.full = full;
         rg.S = a.stages;
         rg.stage_bytes = a.stage_bytes;
-        rg.nrows = (a.n - sl.grp + sl.ngrp - 1) / sl.ngrp;
+        rg.nrows = (rows_of(a) - sl.grp + sl.ngrp - 1) / sl.ngrp;
         rg.copy_bytes = (uint32_t)(((sl.c1 - sl.c0 + VecT<T>::W - 1) / VecT<T>::W) * sizeof(V));
         rg.issued = 0;
         rg.used = 0;
@@ -1100,7 +1112,7 @@ __global__ void __launch_bounds__(NT, (NT > 256 ? 1 : 2)) sk_persistent_kernel(S
         return;
     }
     if constexpr (CL == 1) {
-        const int nbands = (a.n + R - 1) / R;
+        const int nbands = (rows_of(a) + R - 1) / R;
         if (a.resident && nbands <= nblk) {
             load_band_g<T, CH, R, NT>(a, sl, sl.grp, nbands, xres);
             sk_sweeps<T, CH, R, CL, NT, true, false>(a, bar, sl, &xch, xi, k0, K, tol, coef, gmax, xres, nullptr);
@@ -1108,6 +1120,163 @@ __global__ void __launch_bounds__(NT, (NT > 256 ? 1 : 2)) sk_persistent_kernel(S
         }
     }
     sk_sweeps<T, CH, R, CL, NT, false, false>(a, bar, sl, &xch, xi, k0, K, tol, coef, gmax, xres, nullptr);
+}
+
+// ------------------------------------------------------------------ row-sharded sweep
+// Column sums of this block's pass (fixed CTA order, fp64) and its max row deviation.
+template <class T>
+__global__ void __launch_bounds__(kThreads) sk_shard_colsum_kernel(SkArgs a, int pass_blocks, double *send) {
+    if (*(volatile int *)&a.st->done || *(volatile int *)&a.st->pending) return;
+    const int n = a.n, np = a.nblk;
+    const T *cp = static_cast<const T *>(a.colpart);
+    for (int j = blockIdx.x * kThreads + threadIdx.x; j < n; j += gridDim.x * kThreads) {
+        double S = 0.0;
+        for (int b = 0; b < np; ++b) S += (double)__ldcg(cp + (int64_t)b * a.ldp + j);
+        send[j] = S;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        double d = 0.0;
+        for (int b = threadIdx.x; b < pass_blocks; b += 32) d = fmax(d, __ldcg(a.devpart + b));
+        for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
+        if (threadIdx.x == 0) send[n] = d;
+    }
+}
+
+// One CTA: the gathered [world][n+1] rows merged in rank order (identical on every
+// rank), then the stopping rule of sk_sweeps and g_k = g_{k-1} - log(colsum).
+// A column sum that under/overflows (fp32: every entry below the ex2 range) is
+// flagged in bad[] and the sweep is left pending: sk_shard_repair_pass/merge then
+// compute those columns' exact fp64 LSE across all ranks, as sk_exact_col does
+// on one GPU, and finish the sweep.
+constexpr int kShardMergeThreads = 1024;
+__device__ __forceinline__ void shard_finish(SkState *st, int k, int stop, int sweeps, int conv, int slot) {
+    if (stop) { st->done = 1; st->sweeps = sweeps; st->converged = conv; st->slot = slot; }
+    st->pending = 0;
+    st->k = k + 1;
+}
+
+__device__ __forceinline__ double block_max_1024(double v, double *s_red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+    __syncthreads();
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    double r = 0.0;
+    for (int w = 0; w < kShardMergeThreads / 32; ++w) r = fmax(r, s_red[w]);
+    return r;
+}
+
+__global__ void __launch_bounds__(kShardMergeThreads) sk_shard_merge_kernel(SkArgs a, const double *recv, int world,
+                                                                            double tiny, unsigned char *bad) {
+    __shared__ double s_red[kShardMergeThreads / 32];
+    __shared__ int s_bad;
+    SkState *st = a.st;
+    if (*(volatile int *)&st->done || *(volatile int *)&st->pending) return;
+    const int tid = threadIdx.x;
+    const int k = st->k, K = st->max_sweeps, n = a.n;
+    const int64_t ld1 = (int64_t)n + 1;
+    const double tol = st->tol;
+    const bool pre = (k == 0);
+    if (tid == 0) s_bad = 0;
+    double drow = 0.0;
+    for (int r = 0; r < world; ++r) drow = fmax(drow, recv[r * ld1 + n]);
+    int stop = 0, sweeps = 0, conv = 0, slot = 0;
+    if (k >= 2) {
+        if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
+        else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
+    }
+    __syncthreads();
+    if (stop) {
+        if (tid == 0) { st->dev = drow; shard_finish(st, k, stop, sweeps, conv, slot); }
+        return;
+    }
+    double dcol = 0.0;
+    int nbad = 0;
+    const double *gold = gslot(a, k + 1);
+    double *gnew = gslot(a, k);
+    for (int j = tid; j < n; j += kShardMergeThreads) {
+        double S = 0.0;
+        for (int r = 0; r < world; ++r) S += recv[r * ld1 + j];
+        const bool b = !(S > tiny) || !isfinite(S);
+        bad[j] = b;
+        nbad += b;
+        if (b) continue;
+        if (pre) dcol = fmax(dcol, fabs(S - 1.0));
+        else gnew[j] = gold[j] - log(S);
+    }
+    if (nbad) atomicAdd(&s_bad, nbad);
+    dcol = block_max_1024(dcol, s_red);  // includes the barrier that publishes s_bad
+    if (tid != 0) return;
+    if (s_bad) {  // the repair round finishes this sweep
+        st->repaired += s_bad;
+        st->dcol = dcol;
+        st->last_dev = drow;
+        st->pending = 1;
+        return;
+    }
+    if (pre) {
+        const double d0 = fmax(drow, dcol);
+        if (d0 < tol) { stop = 1; sweeps = 0; conv = 1; slot = 0; st->dev = d0; }
+        st->last_dev = d0;
+    }
+    shard_finish(st, k, stop, sweeps, conv, slot);
+}
+
+// Exact column LSE pairs over this block's rows for the flagged columns (fp64):
+// pair[2j] = max_i arg_ij, pair[2j+1] = sum_i exp(arg_ij - max), arg = E_ij (+ f_k,i).
+template <class T>
+__global__ void __launch_bounds__(kThreads) sk_shard_repair_pass_kernel(SkArgs a, const unsigned char *bad,
+                                                                        double *pair) {
+    if (!*(volatile int *)&a.st->pending) return;
+    const int n = a.n, m = rows_of(a), k = a.st->k;
+    const bool pre = (k == 0);
+    const double coef = a.st->coef, gmax = a.st->gmax;
+    const double *f = fslot(a, k);
+    const T *G = static_cast<const T *>(a.G);
+    for (int j = blockIdx.x * kThreads + threadIdx.x; j < n; j += gridDim.x * kThreads) {
+        double M = -INFINITY, S = 0.0;
+        if (bad[j]) {
+            for (int i = 0; i < m; ++i) M = fmax(M, coef * (gmax - (double)G[(int64_t)i * a.ld + j]) + (pre ? 0.0 : f[i]));
+            for (int i = 0; i < m; ++i)
+                S += exp(coef * (gmax - (double)G[(int64_t)i * a.ld + j]) + (pre ? 0.0 : f[i]) - M);
+        }
+        pair[2 * j] = M;
+        pair[2 * j + 1] = S;
+    }
+}
+
+// Rank-order combine of the gathered pairs [world][2n]; finishes the pending sweep.
+__global__ void __launch_bounds__(kShardMergeThreads) sk_shard_repair_merge_kernel(SkArgs a, const double *recv,
+                                                                                   int world, const unsigned char *bad) {
+    __shared__ double s_red[kShardMergeThreads / 32];
+    SkState *st = a.st;
+    if (!*(volatile int *)&st->pending) return;
+    const int tid = threadIdx.x, k = st->k, n = a.n;
+    const bool pre = (k == 0);
+    double *gnew = gslot(a, k);
+    double dcol = 0.0;
+    for (int j = tid; j < n; j += kShardMergeThreads) {
+        if (!bad[j]) continue;
+        double M = -INFINITY;
+        for (int r = 0; r < world; ++r) M = fmax(M, recv[(int64_t)r * 2 * n + 2 * j]);
+        double S = 0.0;
+        for (int r = 0; r < world; ++r) {
+            const double mr = recv[(int64_t)r * 2 * n + 2 * j];
+            if (mr != -INFINITY) S += recv[(int64_t)r * 2 * n + 2 * j + 1] * exp(mr - M);
+        }
+        const double lse = M + log(S);
+        if (pre) dcol = fmax(dcol, fabs(exp(lse) - 1.0));
+        else gnew[j] = -lse;
+    }
+    dcol = block_max_1024(dcol, s_red);
+    if (tid != 0) return;
+    int stop = 0, sweeps = 0, conv = 0, slot = 0;
+    if (pre) {
+        const double d0 = fmax(st->last_dev, fmax(st->dcol, dcol));
+        if (d0 < st->tol) { stop = 1; sweeps = 0; conv = 1; slot = 0; st->dev = d0; }
+        st->last_dev = d0;
+    }
+    shard_finish(st, k, stop, sweeps, conv, slot);
 }
 
 template <class T, int CH, int R>
@@ -1191,7 +1360,7 @@ __global__ void __launch_bounds__(kThreads) sk_emit_kernel(SkArgs a, T *Q, int64
     const double coef = a.st->coef, gmax = a.st->gmax;
     const float ks = (float)SkMath<float>::kScale;
     const float coef2 = (float)(coef * SkMath<float>::kScale);
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int i = blockIdx.x; i < rows_of(a); i += gridDim.x) {
         const double fi = __ldcg(f + i);
         const T *Gi = G + (int64_t)i * a.ld;
         for (int j = threadIdx.x; j < n; j += kThreads) {
@@ -1295,7 +1464,8 @@ cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunch
 
 }  // namespace
 
-template <class T> SkPlan sk_plan(int n, int num_sms) {
+template <class T> SkPlan sk_plan(int n, int num_sms, int mrows) {
+    if (mrows < 0) mrows = n;
     constexpr int VW = VecT<T>::W;
     SkPlan p;
     // Row width per CTA: whole rows when they fit kMaxCh chunks per thread,
@@ -1321,7 +1491,7 @@ template <class T> SkPlan sk_plan(int n, int num_sms) {
     if (p.ch > kMaxCh)
         throw Error(GOAT_ENOTSUP, "sinkhorn: order " + std::to_string(n) + " exceeds 8-CTA clusters of this build");
     p.rows = wide ? 1 : rows_for(p.ch, p.nt);
-    const int nbands = (n + p.rows - 1) / p.rows;
+    const int nbands = (mrows + p.rows - 1) / p.rows;
     // Cluster-split wide rows stream through the bulk-copy ring (measured: +30%
     // at n = 20000-40000); unsplit wide rows keep the register prefetch, which
     // measured faster at n = 10000 (profiles/round1_sk_tune.md).
@@ -1411,14 +1581,56 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
 }
 
 template <class T>
+void sk_launch_shard_pass(const SkArgs &a, const SkPlan &p, unsigned *bar, double *send, cudaStream_t s) {
+    if (!p.persistent) throw Error(GOAT_ENOTSUP, "sharded sinkhorn needs the persistent pass kernel");
+    SkArgs args = a;
+    args.single_pass = 1;
+    sk_launch_persistent<T>(args, p, bar, s);
+    args.nblk = p.ngrp;
+    sk_shard_colsum_kernel<T><<<std::max(1, std::min(ceil_div(a.n, kThreads), 4 * 148)), kThreads, 0, s>>>(
+        args, p.nblk, send);
+    note_launch();
+    GOAT_CHECK_LAUNCH();
+}
+
+template <class T>
+void sk_launch_shard_merge(const SkArgs &a, const double *recv, int world, unsigned char *bad, cudaStream_t s) {
+    const double tiny = sizeof(T) == 4 ? 1e-30 : 1e-290;
+    sk_shard_merge_kernel<<<1, kShardMergeThreads, 0, s>>>(a, recv, world, tiny, bad);
+    note_launch();
+    GOAT_CHECK_LAUNCH();
+}
+
+template <class T> void sk_launch_shard_repair_pass(const SkArgs &a, const unsigned char *bad, double *pair,
+                                                    cudaStream_t s) {
+    sk_shard_repair_pass_kernel<T><<<std::max(1, std::min(ceil_div(a.n, kThreads), 4 * 148)), kThreads, 0, s>>>(
+        a, bad, pair);
+    note_launch();
+    GOAT_CHECK_LAUNCH();
+}
+
+void sk_launch_shard_repair_merge(const SkArgs &a, const double *recv, int world, const unsigned char *bad,
+                                  cudaStream_t s) {
+    sk_shard_repair_merge_kernel<<<1, kShardMergeThreads, 0, s>>>(a, recv, world, bad);
+    note_launch();
+    GOAT_CHECK_LAUNCH();
+}
+
+template <class T>
 void sk_launch_emit(const SkArgs &a, T *Q, int64_t ldq, const T *P, int64_t ldp, const T *L,
                     int64_t ldl, double *part, int nblk, cudaStream_t s) {
     sk_emit_kernel<T><<<nblk, kThreads, 0, s>>>(a, Q, ldq, P, ldp, L, ldl, part); note_launch();
     GOAT_CHECK_LAUNCH();
 }
 
-template SkPlan sk_plan<float>(int, int);
-template SkPlan sk_plan<double>(int, int);
+template SkPlan sk_plan<float>(int, int, int);
+template SkPlan sk_plan<double>(int, int, int);
+template void sk_launch_shard_pass<float>(const SkArgs &, const SkPlan &, unsigned *, double *, cudaStream_t);
+template void sk_launch_shard_pass<double>(const SkArgs &, const SkPlan &, unsigned *, double *, cudaStream_t);
+template void sk_launch_shard_merge<float>(const SkArgs &, const double *, int, unsigned char *, cudaStream_t);
+template void sk_launch_shard_merge<double>(const SkArgs &, const double *, int, unsigned char *, cudaStream_t);
+template void sk_launch_shard_repair_pass<float>(const SkArgs &, const unsigned char *, double *, cudaStream_t);
+template void sk_launch_shard_repair_pass<double>(const SkArgs &, const unsigned char *, double *, cudaStream_t);
 template void sk_launch_pass<float>(const SkArgs &, const SkPlan &, cudaStream_t);
 template void sk_launch_pass<double>(const SkArgs &, const SkPlan &, cudaStream_t);
 template void sk_launch_merge<float>(const SkArgs &, const SkPlan &, cudaStream_t);
