@@ -38,7 +38,8 @@ struct Handle {
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
     // workspace (sized for the largest order seen)
-    int64_t cap_n = 0;
+    int64_t cap_n = 0;    // vectors / scratch sized for this order
+    int64_t cap_mat = 0;  // n x n workspace sized for this order
     DevBuf A, B, P, Q, G, GQ, T1, L, Gl, M;     // element = precision
     DevBuf A64, B64, stage;                     // fp64 inputs (objective) + upload staging
     DevBuf f[2], g[2], colpart, devpart, devcol, state, red, scal, vec, ivec;
@@ -77,13 +78,18 @@ inline int64_t ld_for(int64_t n) { return round_up(std::max<int64_t>(n, 1), 8); 
 // assignments match scipy even under ties); above it the auction front end.
 constexpr int kAuctionMinN = 256;
 
-void ensure_workspace(Handle &h, int64_t n) {
+// matrices = false: vectors, reduction scratch and LAP state only (the row-sharded
+// primitives keep their own blocks; a full n x n buffer per rank would defeat sharding).
+void ensure_workspace(Handle &h, int64_t n, bool matrices = true) {
     GOAT_CUDA(cudaSetDevice(h.device));
-    if (n <= h.cap_n) return;
     const int64_t ld = ld_for(n);
     const size_t es = h.precision == GOAT_FP32 ? 4 : 8;
     const size_t mat = (size_t)n * ld * es;
-    for (DevBuf *b : {&h.A, &h.B, &h.P, &h.Q, &h.G, &h.GQ, &h.T1, &h.M}) b->ensure(mat);
+    if (matrices && n > h.cap_mat) {
+        for (DevBuf *b : {&h.A, &h.B, &h.P, &h.Q, &h.G, &h.GQ, &h.T1, &h.M}) b->ensure(mat);
+        h.cap_mat = n;
+    }
+    if (n <= h.cap_n) return;
     const size_t vec = (size_t)ld * 8;
     for (int s = 0; s < 2; ++s) { h.f[s].ensure(vec); h.g[s].ensure(vec); }
     h.vec.ensure(vec * 4);
@@ -412,6 +418,24 @@ LotOut run_lot(Ctx &c, const T *Gin, int sense, double lam, int max_sweeps, doub
     return out;
 }
 
+struct Timer {
+    cudaEvent_t a, b;
+    cudaStream_t s;
+    explicit Timer(cudaStream_t st) : s(st) {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+    }
+    double stop() {
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        return ms;
+    }
+    ~Timer() { cudaEventDestroy(a); cudaEventDestroy(b); }
+};
+
 // ------------------------------------------------------------------ LAP
 template <class T>
 int run_lap(Ctx &c, const T *M, int sense, int *perm_dev, std::vector<int> &perm_host) {
@@ -456,10 +480,18 @@ int run_lap(Ctx &c, const T *M, int sense, int *perm_dev, std::vector<int> &perm
             GOAT_CUDA(cudaMemcpyAsync(h.lap_stats, aw.counters, 16, cudaMemcpyDeviceToHost, c.s));
             warm = 1;
         }
+        const bool verbose = getenv("GOAT_LAP_VERBOSE") != nullptr;
+        if (verbose) {
+            sync(c);
+            fprintf(stderr, "lap n=%d auction: assigned %d rounds %d capped %d freed %d\n", n, h.lap_stats[0],
+                    h.lap_stats[1], h.lap_stats[2], h.lap_stats[3]);
+        }
+        Timer tsap(c.s);
         launch_lap_sap<T>(M, c.ld, n, sense, w, c.s, warm);
         int status = 0;
         GOAT_CUDA(cudaMemcpyAsync(&status, w.status, sizeof(int), cudaMemcpyDeviceToHost, c.s));
         sync(c);
+        if (verbose) fprintf(stderr, "lap n=%d augmenting-path repair: %.1f ms\n", n, tsap.stop());
         if (status != 0) throw Error(GOAT_EINVAL, "cost matrix is infeasible");
     }
     perm_host.resize(n);
@@ -480,23 +512,6 @@ double alpha_opt(double c2, double c1, int sense) {
     return end <= 0.0 ? 1.0 : 0.0;
 }
 
-struct Timer {
-    cudaEvent_t a, b;
-    cudaStream_t s;
-    explicit Timer(cudaStream_t st) : s(st) {
-        cudaEventCreate(&a);
-        cudaEventCreate(&b);
-        cudaEventRecord(a, s);
-    }
-    double stop() {
-        cudaEventRecord(b, s);
-        cudaEventSynchronize(b);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, a, b);
-        return ms;
-    }
-    ~Timer() { cudaEventDestroy(a); cudaEventDestroy(b); }
-};
 
 // Core loop on device-resident inputs in the workspace (A, B, optional L, P = P0).
 template <class T>
@@ -1197,7 +1212,7 @@ int goat_shard_setup(goat_handle *h, int64_t n, int64_t m, const void *dA_rows, 
         check_order(n);
         require(m >= 1 && m <= n, "block rows must be in [1, n]");
         require(ld >= n, "leading dimension < n");
-        ensure_workspace(*h, n);
+        ensure_workspace(*h, n, false);
         auto &S = h->sh;
         S.ready = false;
         S.n = n; S.m = m; S.sym = (dAT_rows == nullptr); S.fill = false;
@@ -1411,11 +1426,12 @@ int goat_lap_device(goat_handle *h, int64_t n, const void *dM, int64_t ldm, int3
         check_order(n);
         require(ldm >= n, "leading dimension < n");
         require(sense == GOAT_MINIMIZE || sense == GOAT_MAXIMIZE, "sense must be minimize or maximize");
-        ensure_workspace(*h, n);
+        ensure_workspace(*h, n, false);
         dispatch(*h, [&](auto *tag) {
             using T = std::remove_pointer_t<decltype(tag)>;
             Ctx c(*h, (int)n);
             const size_t es = sizeof(T);
+            h->M.ensure((size_t)n * c.ld * es);
             GOAT_CUDA(cudaMemsetAsync(h->M.p, 0, (size_t)n * c.ld * es, c.s));
             GOAT_CUDA(cudaMemcpy2DAsync(h->M.p, c.ld * es, dM, ldm * es, n * es, n, cudaMemcpyDeviceToDevice, c.s));
             std::vector<int> ph;
