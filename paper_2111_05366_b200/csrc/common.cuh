@@ -80,6 +80,7 @@ struct SkState {
     int max_sweeps;
     int log_mode;
     double dcol;    // row-sharded pre-check: column deviation of the columns that needed no repair
+    int redone;     // wide fp32 rows: sweeps recomputed with the max shift (diagnostic)
 };
 
 // Count of kernels this library launched (reported as gpu_launches).

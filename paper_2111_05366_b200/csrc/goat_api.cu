@@ -1101,6 +1101,11 @@ int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int3
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
             *ms_per_sweep = ms / (reps + 2);
+            if (getenv("GOAT_SK_VERBOSE")) {
+                GOAT_CUDA(cudaMemcpy(h->h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost));
+                fprintf(stderr, "bench_sweep n=%d cl=%d ch=%d pipe=%d stages=%d sweeps=%d redone=%d\n", (int)n, plan.cl,
+                        plan.ch, (int)plan.pipe, plan.stages, h->h_state->sweeps, h->h_state->redone);
+            }
         });
     });
 }

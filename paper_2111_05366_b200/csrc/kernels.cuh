@@ -45,6 +45,7 @@ struct SkPlan {
     int stages = 0;           // wide rows: bulk-copy ring depth (0 = register prefetch)
     int stage_bytes = 0;
     size_t smem = 0;          // dynamic shared memory of the persistent kernel
+    bool pipe = false;        // wide fp32 rows: decoupled bulk-copy pipeline (sk_pipe_kernel)
 };
 
 // rows: rows of a row-sharded block (-1 = n).

@@ -142,12 +142,17 @@ __device__ __forceinline__ void xbar_arm(uint64_t *bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
+// CTA-scope acquire: the exchanged data lives in this CTA's shared memory and is
+// published by the mbarrier's complete_tx.  (A cluster-scope acquire compiles to
+// CCTL.IVALL -- an L1 invalidation on every completed wait -- which measured as
+// the dominant stall of the wide-row kernels: every spill and stack reload then
+// went to L2.)
 __device__ __forceinline__ void xbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "XW_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
         "@!P1 bra XW_%=;\n"
         "}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
         "r"(parity)
@@ -900,16 +905,18 @@ __device__ __forceinline__ void pass_body_tma(const SkArgs &a, int k, int max_sw
 // Exact column LSE for a column whose partial sum under/overflowed:
 // g_j = -LSE_i(E_ij + f_i) over all rows (fp64).  Rare repair path.
 template <class T>
-__device__ __noinline__ double sk_exact_col(const SkArgs &a, int j, const double *f, bool pre, double coef, double gmax) {
-    const T *G = static_cast<const T *>(a.G);
+__device__ __noinline__ double sk_exact_col(const T *G, int64_t ld, int n, int j, const double *f, bool pre, double coef,
+                                            double gmax) {
+    // (fields passed by value: a reference to the kernel's SkArgs would force a
+    // per-thread stack copy of it)
     double M = -INFINITY;
-    for (int i = 0; i < a.n; ++i) {
-        const double e = coef * (gmax - (double)G[(int64_t)i * a.ld + j]) + (pre ? 0.0 : __ldcg(f + i));
+    for (int i = 0; i < n; ++i) {
+        const double e = coef * (gmax - (double)G[(int64_t)i * ld + j]) + (pre ? 0.0 : __ldcg(f + i));
         M = fmax(M, e);
     }
     double S = 0.0;
-    for (int i = 0; i < a.n; ++i) {
-        const double e = coef * (gmax - (double)G[(int64_t)i * a.ld + j]) + (pre ? 0.0 : __ldcg(f + i));
+    for (int i = 0; i < n; ++i) {
+        const double e = coef * (gmax - (double)G[(int64_t)i * ld + j]) + (pre ? 0.0 : __ldcg(f + i));
         S += exp(e - M);
     }
     return -(M + log(S));
@@ -946,13 +953,13 @@ __device__ __forceinline__ void merge_body(const SkArgs &a, int k, double coef, 
         for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
         if (lane != 0) continue;
         if (pre) {
-            if (!(S > tiny)) S = exp(-sk_exact_col<T>(a, j, nullptr, true, coef, gmax));
+            if (!(S > tiny)) S = exp(-sk_exact_col<T>(static_cast<const T *>(a.G), a.ld, a.n, j, nullptr, true, coef, gmax));
             dloc = fmax(dloc, fabs(S - 1.0));
         } else {
             const double gold = __ldcg(gslot(a, k + 1) + j);
             double gnew = gold - log(S);
             if (!(S > tiny) || !isfinite(S)) {
-                gnew = sk_exact_col<T>(a, j, fslot(a, k), false, coef, gmax);
+                gnew = sk_exact_col<T>(static_cast<const T *>(a.G), a.ld, a.n, j, fslot(a, k), false, coef, gmax);
                 atomicAdd(&a.st->repaired, 1);
             }
             __stcg(gslot(a, k) + j, gnew);
@@ -1120,6 +1127,414 @@ __global__ void __launch_bounds__(NT, (NT > 256 ? 1 : 2)) sk_persistent_kernel(S
         }
     }
     sk_sweeps<T, CH, R, CL, NT, false, false>(a, bar, sl, &xch, xi, k0, K, tol, coef, gmax, xres, nullptr);
+}
+
+// ------------------------------------------------------------------ decoupled wide-row pipeline (fp32)
+// Wide rows (one row per band) without a block barrier per band.  Row slices
+// stream through a ring of S shared-memory stages (cp.async.bulk, full/empty
+// mbarriers), and the three steps of a band are lagged so no warp waits on the
+// latency of another step:
+//   band b   : every warp reduces its columns of the row -> a (max, sum) pair
+//              per warp, kept exponentials y_b in registers, arrives on wbar[b];
+//   band b+1 : warp 0 combines the NW warp pairs (fixed tree) into the CTA pair
+//              and sends it to every cluster rank (st.async + complete_tx);
+//   band b+LAG: every warp combines the CL rank pairs in rank order -> row LSE ->
+//              f_b, the deviation, and the column contributions acc += y_b * sc.
+// LAG = 1 without a cluster (the CTA pair is local), 2 with one (the peers' pairs
+// get a whole band to arrive).  Results are bit-identical to a lock-step order:
+// every reduction tree is fixed.  A stage is refilled as soon as every warp has
+// loaded it (empty barrier); the ring runs ahead across sweeps.
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cta(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "MW_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra MW_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int NW, int CL> struct PipeSm {
+    uint64_t full[8], empty[8], wbar[4], xbar[4];
+    float wp[4][NW][2];  // per-warp (max, sum) of a band slot
+    float xp[4][CL][2];  // per-rank CTA (max, sum) of a band slot
+};
+
+struct PipeRing {
+    char *base;
+    int S, stage_bytes, nrows;
+    uint32_t copy_bytes;
+    unsigned issued;  // bands issued (thread 0)
+    unsigned used;    // bands consumed (all threads)
+};
+
+// Thread 0: issue every band below `upto` whose stage has been released.
+template <int NW, int CL>
+__device__ __forceinline__ void pipe_produce(const SkArgs &a, const Slice &sl, PipeRing &rg, PipeSm<NW, CL> &ps,
+                                             unsigned upto) {
+    while (rg.issued < upto) {
+        if (a.single_pass && rg.issued >= (unsigned)rg.nrows) return;  // one sweep per launch
+        const unsigned u = rg.issued;
+        const int s = (int)(u % (unsigned)rg.S);
+        if (u >= (unsigned)rg.S) mbar_wait_cta(&ps.empty[s], ((u / (unsigned)rg.S) - 1) & 1);
+        const int row = sl.grp + (int)(u % (unsigned)rg.nrows) * sl.ngrp;
+        const float *src = static_cast<const float *>(a.G) + (int64_t)row * a.ld + sl.c0;
+        xbar_arm(&ps.full[s], rg.copy_bytes);
+        bulk_g2s(rg.base + (size_t)s * rg.stage_bytes, src, rg.copy_bytes, &ps.full[s]);
+        ++rg.issued;
+    }
+}
+
+// Row shift of the exponentials.  MAXP (pre-check, sweep 1, single-pass
+// launches, and any sweep redone after an out-of-range row): the warp/CTA/cluster
+// row maximum, combined as (max, sum) pairs.  Otherwise the previous sweep's row
+// LSE, -f_{k-1,i}: the exponent of every term is then bounded by the change of
+// the row's LSE, no max reduction is needed, and the pairs reduce to plain sums.
+// A row whose sum leaves [2^-40, 2^100] (early sweeps: g moved by > 40 log2
+// units) sets the redo flag and the whole sweep is recomputed with MAXP.
+constexpr int kPipeShiftRows = 4096;
+constexpr float kShiftLo = 9.094947e-13f;   // 2^-40
+constexpr float kShiftHi = 1.2676506e30f;   // 2^100
+
+// Finish a band: f_k of the row (writer), the pre-check deviation, and the column
+// contributions acc += y * 2^(m_warp - lse) of this warp's exponentials.
+#define PIPE_FINISH(ITF, LSE, MWARP, YV)                                                        \
+    do {                                                                                        \
+        const double lse_ = (LSE);                                                              \
+        if (writer) {                                                                           \
+            const double fnew = -lse_ * (1.0 / SkMath<T>::kScale);                              \
+            if (pre) devmax = fmax(devmax, SkMath<T>::dev(-fnew));                              \
+            else __stcg(fout + sl.grp + (ITF) * sl.ngrp, fnew);                                 \
+        }                                                                                       \
+        if (!rowonly && (MWARP) != neg_inf<T>()) {                                              \
+            const T sc = SkMath<T>::ex((T)((double)(MWARP) + (pre ? 0.0 : -lse_)));             \
+            _Pragma("unroll") for (int c = 0; c < CH; ++c)                                      \
+                _Pragma("unroll") for (int e = 0; e < VW; ++e) acc[c][e] += (YV)[c][e] * sc;   \
+        }                                                                                       \
+    } while (0)
+
+template <int CH, int CL, int NT, bool MAXP>
+__device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
+                                               const Slice &sl, PipeSm<NT / 32, CL> &ps, PipeRing &rg,
+                                               unsigned *redo) {
+    using T = float;
+    using V = float4;
+    constexpr int VW = 4;
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool pre = (k == 0);
+    const bool rowonly = (k == max_sweeps + 1);
+    const double *gin = gslot(a, k + 1);
+    const double *fprev = fslot(a, k + 1);
+    double *fout = fslot(a, k);
+    const double ks = SkMath<T>::kScale;
+    const T coef = (T)(coef_d * ks);
+    const T gmax = (T)gmax_d;
+    const int c0 = sl.c0, c1 = sl.c1;
+    const bool writer = (sl.rank == 0) && warp == 0 && lane == 0;
+    const int S = rg.S;
+
+    // g of this thread's columns (scaled; -inf masks columns past the slice) lives
+    // in shared memory after the ring: registers hold only the exponentials and
+    // the column accumulators
+    T acc[CH][VW];
+    V *s_gl = reinterpret_cast<V *>(rg.base + (size_t)rg.S * rg.stage_bytes);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        T gv[VW];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+            const int col = c0 + (tid + NT * c) * VW + e;
+            gv[e] = col < c1 ? ((!pre) ? (T)(__ldcg(gin + col) * ks) : T(0)) : neg_inf<T>();
+            acc[c][e] = T(0);
+        }
+        s_gl[tid + NT * c] = make_float4(gv[0], gv[1], gv[2], gv[3]);  // read back by this thread only
+    }
+    // lagged state (clusters): the previous band's exponentials and warp max
+    constexpr bool LAGGED = CL > 1;
+    T yp[CH][VW];
+    T mp = neg_inf<T>();
+    double devmax = 0.0;  // pre-check only (writer thread)
+    __shared__ T s_wp[2][NW][2];
+    __shared__ float s_shift[MAXP ? 1 : kPipeShiftRows];
+    bool bad = false;
+    if constexpr (!MAXP) {
+        for (int i = tid; i < rg.nrows; i += NT) s_shift[i] = (float)(-__ldcg(fprev + sl.grp + i * sl.ngrp) * ks);
+        __syncthreads();
+    }
+
+    const int nrows = rg.nrows;
+    const unsigned b0 = rg.used;
+    for (int it = 0; it < nrows + (LAGGED ? 1 : 0); ++it) {
+        const unsigned b = b0 + (unsigned)it;
+        // keep S - 1 bands in flight beyond the one being loaded (never blocks in
+        // steady state: every warp passed the block barrier of band b - 1)
+        if (tid == 0) pipe_produce<NW, CL>(a, sl, rg, ps, b + (unsigned)S - 1);
+        T y[CH][VW];
+        T m = neg_inf<T>();
+        if (it < nrows) {
+            const int s = (int)(b % (unsigned)S);
+            mbar_wait_cta(&ps.full[s], (b / (unsigned)S) & 1);
+            const V *st = reinterpret_cast<const V *>(rg.base + (size_t)s * rg.stage_bytes);
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int col = c0 + (tid + NT * c) * VW;
+                V xv;
+                if (col < c1) xv = st[tid + NT * c];
+                else xv = make_float4(0.f, 0.f, 0.f, 0.f);
+                y[c][0] = xv.x; y[c][1] = xv.y; y[c][2] = xv.z; y[c][3] = xv.w;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ps.empty[s]);
+            if constexpr (MAXP) {
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const V g4 = s_gl[tid + NT * c];
+                    const T gl[VW] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) {
+                        const T arg = coef * (gmax - y[c][e]) + gl[e];  // E_ij + g_j (sinkhorn.py:125)
+                        y[c][e] = arg;
+                        m = vmax(m, arg);
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) m = vmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+            } else {
+                m = s_shift[it];  // the row's shift, identical in every warp and cluster rank
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const V g4 = s_gl[tid + NT * c];
+                    const T gl[VW] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) y[c][e] = coef * (gmax - y[c][e]) + gl[e];
+                }
+            }
+            const T mx = (m == neg_inf<T>()) ? T(0) : m;
+            T sp[VW];
+#pragma unroll
+            for (int e = 0; e < VW; ++e) sp[e] = T(0);
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+                for (int e = 0; e < VW; ++e) {
+                    const T v = SkMath<T>::ex(y[c][e] - mx);
+                    y[c][e] = v;
+                    sp[e] += v;
+                }
+            T sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+            if (lane == 0) { s_wp[b & 1][warp][0] = m; s_wp[b & 1][warp][1] = sum; }
+            __syncthreads();
+            // every warp combines the NW warp pairs (fixed tree: identical in all warps)
+            T M, Sm;
+            if constexpr (MAXP) {
+                const T mv = lane < NW ? s_wp[b & 1][lane][0] : neg_inf<T>();
+                M = mv;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) M = vmax(M, __shfl_xor_sync(0xffffffffu, M, off));
+                Sm = (mv != neg_inf<T>()) ? s_wp[b & 1][lane][1] * SkMath<T>::ex(mv - M) : T(0);
+            } else {
+                M = m;
+                Sm = lane < NW ? s_wp[b & 1][lane][1] : T(0);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) Sm += __shfl_xor_sync(0xffffffffu, Sm, off);
+            if constexpr (!LAGGED) {
+                if constexpr (!MAXP) bad |= !(Sm >= kShiftLo && Sm <= kShiftHi);
+                PIPE_FINISH(it, (double)M + SkMath<T>::lgt(Sm), m, y);
+            } else {
+                // this CTA's pair -> every rank of the cluster; finished next band
+                const int xs = (int)(b & 3);
+                if (warp == 0) {
+                    if (lane == 0) xbar_arm(&ps.xbar[xs], (uint32_t)(CL * 2 * sizeof(T)));
+                    __syncwarp();
+                    if (lane < CL)
+                        st_async_pair(dsmem_map(&ps.xp[xs][sl.rank][0], lane), M, Sm, dsmem_map(&ps.xbar[xs], lane));
+                }
+            }
+        }
+        if constexpr (LAGGED) {
+            if (it >= 1) {
+                const unsigned bf = b - 1;
+                const int xs = (int)(bf & 3);
+                T mq[CL], sq[CL];
+                if (lane == 0) {
+                    xbar_wait(&ps.xbar[xs], (bf >> 2) & 1);
+#pragma unroll
+                    for (int q = 0; q < CL; ++q) { mq[q] = ps.xp[xs][q][0]; sq[q] = ps.xp[xs][q][1]; }
+                }
+#pragma unroll
+                for (int q = 0; q < CL; ++q) {
+                    mq[q] = __shfl_sync(0xffffffffu, mq[q], 0);
+                    sq[q] = __shfl_sync(0xffffffffu, sq[q], 0);
+                }
+                T M = neg_inf<T>(), Sm = T(0);
+                if constexpr (MAXP) {
+#pragma unroll
+                    for (int q = 0; q < CL; ++q) M = vmax(M, mq[q]);
+#pragma unroll
+                    for (int q = 0; q < CL; ++q)
+                        if (mq[q] != neg_inf<T>()) Sm += sq[q] * SkMath<T>::ex(mq[q] - M);
+                } else {
+                    M = mq[0];  // the common shift
+#pragma unroll
+                    for (int q = 0; q < CL; ++q) Sm += sq[q];
+                    bad |= !(Sm >= kShiftLo && Sm <= kShiftHi);
+                }
+                PIPE_FINISH(it - 1, (double)M + SkMath<T>::lgt(Sm), mp, yp);
+            }
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+                for (int e = 0; e < VW; ++e) yp[LAGGED ? c : 0][e] = y[c][e];
+            mp = m;
+        }
+    }
+    rg.used = b0 + (unsigned)nrows;
+    if (!rowonly) {
+        T *cp = static_cast<T *>(a.colpart) + (int64_t)sl.grp * a.ldp;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int col = c0 + (tid + NT * c) * VW;
+            if (col < c1) __stcg(reinterpret_cast<V *>(cp + col), make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]));
+        }
+    }
+    if constexpr (!MAXP) {
+        if (bad && tid == 0) atomicOr(redo, 1u);  // `bad` is uniform across the CTA
+    }
+    // dev_{k-1} = max over this group's rows of |expm1(f_{k-1} - f_k)| = |u K v - 1|
+    __shared__ double s_dev[NW];
+    if (sl.rank == 0 && k >= 2) {
+        __syncthreads();  // the writer's f_k stores precede the reads below
+        for (int i = tid; i < nrows; i += NT) {
+            const int row = sl.grp + i * sl.ngrp;
+            devmax = fmax(devmax, SkMath<T>::dev(__ldcg(fprev + row) - __ldcg(fout + row)));
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) devmax = fmax(devmax, __shfl_xor_sync(0xffffffffu, devmax, off));
+    if (lane == 0) s_dev[warp] = devmax;
+    __syncthreads();
+    if (tid == 0) {
+        double d = 0.0;
+        for (int w = 0; w < NW; ++w) d = fmax(d, s_dev[w]);
+        __stcg(a.devpart + blockIdx.x, d);
+        if (a.dslot) atomicMax(a.dslot + (k & 1), (unsigned long long)__double_as_longlong(d));
+    }
+}
+
+__device__ __forceinline__ bool env_shift_ok(const SkArgs &a) { return a.resident != 2; }  // resident==2: force max
+
+template <int CH, int CL, int NT>
+__global__ void __launch_bounds__(NT, 1) sk_pipe_kernel(SkArgs a, unsigned *bar) {
+    using T = float;
+    constexpr int NW = NT / 32;
+    __shared__ int s_k, s_done;
+    if (threadIdx.x == 0) { s_k = a.st->k; s_done = a.st->done | a.st->pending; }
+    __syncthreads();
+    if (a.single_pass && s_done) return;
+    const int k0 = s_k;
+    const int K = a.st->max_sweeps;
+    const double tol = a.st->tol, coef = a.st->coef, gmax = a.st->gmax;
+    const int blk = blockIdx.x, nblk = gridDim.x;
+    Slice sl{0, a.n, blk, nblk, 0};
+    if constexpr (CL > 1) {
+        uint32_t rank, cid, ncl;
+        asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+        asm("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
+        sl.rank = (int)rank;
+        sl.grp = (int)cid;
+        sl.ngrp = (int)ncl;
+        sl.c0 = min(a.n, (int)rank * a.slice_w);
+        sl.c1 = min(a.n, sl.c0 + a.slice_w);
+    }
+    __shared__ PipeSm<NW, CL> ps;
+    extern __shared__ __align__(128) char sk_ring[];
+    PipeRing rg;
+    rg.base = sk_ring;
+    rg.S = a.stages;
+    rg.stage_bytes = a.stage_bytes;
+    rg.nrows = (rows_of(a) - sl.grp + sl.ngrp - 1) / sl.ngrp;
+    rg.copy_bytes = (uint32_t)(((sl.c1 - sl.c0 + 3) / 4) * sizeof(float4));
+    rg.issued = 0;
+    rg.used = 0;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < rg.S; ++q) { mbar_init(&ps.full[q], 1); mbar_init(&ps.empty[q], NW); }
+        for (int q = 0; q < 4; ++q) { mbar_init(&ps.wbar[q], NW); mbar_init(&ps.xbar[q], 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if constexpr (CL > 1) cluster_sync();  // every peer's barriers exist before the first st.async
+    else __syncthreads();
+    if (rg.nrows <= 0) rg.nrows = 0;
+    unsigned epoch = 0;
+    auto drain = [&]() {  // no bulk copy may be in flight when the CTA exits
+        if (threadIdx.x == 0)
+            for (unsigned u = rg.used; u < rg.issued; ++u)
+                mbar_wait_cta(&ps.full[u % (unsigned)rg.S], (u / (unsigned)rg.S) & 1);
+        if constexpr (CL > 1) cluster_sync();
+    };
+    // redo flags (one per sweep parity) share the barrier scratch: bytes [256, 264)
+    unsigned *redo = bar + 64;
+    const bool shift_ok = rg.nrows <= kPipeShiftRows && !a.single_pass && env_shift_ok(a);
+    for (int k = k0;; ++k) {
+        bool maxp = !shift_ok || k <= 1;
+        for (;;) {
+            if (rg.nrows > 0) {
+                if (maxp) pass_body_pipe<CH, CL, NT, true>(a, k, K, coef, gmax, sl, ps, rg, redo + (k & 1));
+                else pass_body_pipe<CH, CL, NT, false>(a, k, K, coef, gmax, sl, ps, rg, redo + (k & 1));
+            } else if (threadIdx.x == 0) {
+                __stcg(a.devpart + blockIdx.x, 0.0);
+            }
+            if (a.single_pass) { drain(); return; }
+            grid_barrier(bar, nblk, epoch);
+            if (maxp || !__ldcg(redo + (k & 1))) break;
+            // a row left the shift window: recompute the sweep with the max shift
+            if (blk == 0 && threadIdx.x == 0) { a.dslot[k & 1] = 0ull; a.st->redone += 1; }
+            grid_barrier(bar, nblk, epoch);
+            maxp = true;
+        }
+        const double drow = __longlong_as_double((long long)__ldcg(a.dslot + (k & 1)));
+        if (blk == 0 && threadIdx.x == 0) {
+            a.dslot[(k + 1) & 1] = 0ull;  // next sweep's slots
+            redo[(k + 1) & 1] = 0u;
+        }
+        int stop = 0, sweeps = 0, conv = 0, slot = 0;
+        if (k >= 2) {
+            if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
+            else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
+        }
+        if (!stop) {
+            merge_body<T, NT>(a, k, coef, gmax, blk, nblk);
+            grid_barrier(bar, nblk, epoch);
+            if (k == 0) {
+                const double d0 = fmax(drow, __longlong_as_double((long long)__ldcg(a.dslot + 2)));
+                if (d0 < tol) { stop = 1; sweeps = 0; conv = 1; slot = 0; }
+                if (blk == 0 && threadIdx.x == 0) a.st->last_dev = d0;
+                if (stop && blk == 0 && threadIdx.x == 0) a.st->dev = d0;
+            }
+        } else if (blk == 0 && threadIdx.x == 0) {
+            a.st->dev = drow;
+        }
+        if (stop) {
+            if (blk == 0 && threadIdx.x == 0) {
+                a.st->done = 1; a.st->sweeps = sweeps; a.st->converged = conv; a.st->slot = slot;
+                a.st->k = k + 1;
+            }
+            drain();
+            return;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ row-sharded sweep
@@ -1464,10 +1879,98 @@ cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunch
 
 }  // namespace
 
+template <int CH, int CL> void *pipe_fn() { return (void *)sk_pipe_kernel<CH, CL, kWideThreads>; }
+
+void *pipe_for(int ch, int cl, int nt) {
+#define GOAT_PCL(C)                                       \
+    if (nt == kWideThreads && cl == C) {                  \
+        switch (ch) {                                     \
+            case 3: return pipe_fn<3, C>();               \
+            case 4: return pipe_fn<4, C>();               \
+            case 5: return pipe_fn<5, C>();               \
+            case 6: return pipe_fn<6, C>();               \
+        }                                                 \
+    }
+    GOAT_PCL(1)
+    GOAT_PCL(2)
+    GOAT_PCL(4)
+    GOAT_PCL(8)
+#undef GOAT_PCL
+    throw Error(GOAT_ENOTSUP, "sinkhorn: no pipelined kernel for chunks=" + std::to_string(ch) + " cluster=" +
+                                  std::to_string(cl));
+}
+
+// Wide fp32 rows: the decoupled bulk-copy pipeline (sk_pipe_kernel), one
+// 512-thread CTA per SM, clusters of 2/4/8 once a row exceeds 6 chunks/thread.
+bool pipe_plan(int n, int mrows, SkPlan &p) {
+    constexpr int VW = 4;
+    p.nt = kWideThreads;
+    p.cl = 1;
+    p.slice_w = (int)round_up(n, 8 * VW);
+    p.ch = std::max(3, ceil_div(ceil_div(n, VW), p.nt));
+    if (p.ch > env_int("GOAT_SK_PIPE_CH1", 6)) {
+        // Clustered pipeline: correct, but measured slower than the lock-step
+        // cluster kernel (sk_persistent_kernel, TMA ring) at n = 16384-65536 --
+        // the lagged band needs two exponential sets in registers and spills.
+        // Opt in with GOAT_SK_PIPE=2 (profiles/round1_sk_pipe.md).
+        if (env_int("GOAT_SK_PIPE", 1) != 2) return false;
+        const int maxch = std::min(6, env_int("GOAT_SK_PIPE_CH", 5));
+        while (p.cl < 8) {
+            p.cl *= 2;
+            p.slice_w = (int)round_up(ceil_div(n, p.cl), 8 * VW);
+            p.ch = std::max(3, ceil_div(ceil_div(p.slice_w, VW), p.nt));
+            if (p.ch <= maxch) break;
+        }
+        if (p.ch > 6) return false;
+    }
+    p.rows = 1;
+    p.pipe = true;
+    // ring stages + one more slice for g (scaled), within ~216 KB of dynamic smem
+    p.stage_bytes = (int)round_up((size_t)p.slice_w * sizeof(float), 128);
+    const size_t gl_bytes = (size_t)p.nt * p.ch * 16;  // every thread's chunks, masked ones included
+    p.stages = std::min(8, (int)((216 * 1024 - gl_bytes) / p.stage_bytes));
+    if (const int st = env_int("GOAT_SK_STAGES", 0)) p.stages = std::min(p.stages, std::max(3, st));
+    if (p.stages < 3) return false;
+    p.smem = (size_t)p.stages * p.stage_bytes + gl_bytes;
+    (void)mrows;
+    return true;
+}
+
 template <class T> SkPlan sk_plan(int n, int num_sms, int mrows) {
     if (mrows < 0) mrows = n;
     constexpr int VW = VecT<T>::W;
     SkPlan p;
+    if (sizeof(T) == 4 && ceil_div(ceil_div(n, VW), kThreads) > kMaxCh && env_int("GOAT_SK_PIPE", 1) &&
+        pipe_plan(n, mrows, p)) {
+        void *const kfn = pipe_for(p.ch, p.cl, p.nt);
+        GOAT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+        if (p.cl > 1) GOAT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        p.persistent = true;
+        int groups = 0;
+        if (p.cl == 1) {
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)kfn, p.nt, p.smem);
+            groups = std::max(1, occ) * num_sms;
+        } else {
+            cudaLaunchAttribute attrs[2];
+            SkPlan q = p;
+            q.nblk = p.cl * num_sms;
+            cudaLaunchConfig_t cfg = persistent_config(q, nullptr, attrs);
+            cudaLaunchAttribute cattr = attrs[1];
+            cfg.attrs = &cattr;
+            cfg.numAttrs = 1;
+            int ncl = 0;
+            GOAT_CUDA(cudaOccupancyMaxActiveClusters(&ncl, kfn, &cfg));
+            groups = std::max(1, ncl);
+        }
+        int ngrp = std::max(1, std::min(mrows, groups));
+        if (const int force = env_int("GOAT_SK_BLOCKS", 0)) ngrp = std::max(1, std::min({force / p.cl, mrows, groups}));
+        p.ngrp = ngrp;
+        p.nblk = ngrp * p.cl;
+        p.merge_blocks = std::max(1, std::min((n + 7) / 8, 4 * num_sms));
+        p.colpart_bytes = (size_t)std::max(p.nblk, num_sms * 2) * round_up(n, 8) * sizeof(T);
+        return p;
+    }
     // Row width per CTA: whole rows when they fit kMaxCh chunks per thread,
     // else a cluster of cl CTAs splits each row into column slices.
     p.cl = 1;
@@ -1575,7 +2078,7 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
     void *params[] = {&args, &bar};
     cudaLaunchAttribute attrs[2];
     cudaLaunchConfig_t cfg = persistent_config(p, s, attrs);
-    void *fn = persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
+    void *fn = p.pipe ? pipe_for(p.ch, p.cl, p.nt) : persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
     GOAT_CUDA(cudaLaunchKernelExC(&cfg, fn, params));
     note_launch();
 }

@@ -31,7 +31,7 @@ def run(n, prec, env, sweeps):
     r = subprocess.run([sys.executable, "-c", CODE.format(n=n, prec=prec, sweeps=sweeps)], env=e,
                        capture_output=True, text=True, timeout=600)
     try:
-        return float(r.stdout.strip().splitlines()[-1]), None
+        return float(r.stdout.strip().splitlines()[-1]), (r.stderr.strip().splitlines() or [None])[-1]
     except Exception:
         return None, r.stderr[-400:]
 
