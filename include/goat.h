@@ -108,6 +108,32 @@ int goat_fw_core_device(goat_handle *h, int64_t n,
                         const void *dL, int64_t ldl, const void *dP0, int64_t ldp,
                         const goat_options *opts, goat_fw_result *res);
 
+/* Sparse adjacency (CSR).  Rows hold strictly increasing column indices; values
+ * NULL means every stored entry is 1 (an unweighted graph).  Host calls take
+ * float64 values; the _device variants take device pointers whose values have
+ * the handle's element type.  The reference has no sparse input path (core.py:22
+ * densifies everything); these entries replace _fw_core (matcher.py:177-212) and
+ * gradient (matcher.py:100-107) for graphs held as CSR (BASELINE config 5). */
+typedef struct goat_csr {
+    const int64_t *rowptr;  /* [n+1], rowptr[0] = 0, rowptr[n] = nnz */
+    const int32_t *colidx;  /* [nnz] */
+    const void *values;     /* [nnz] or NULL */
+    int64_t nnz;
+} goat_csr;
+
+int goat_fw_core_csr(goat_handle *h, int64_t n, const goat_csr *A, const goat_csr *B,
+                     const double *L, int64_t ldl, const double *P0, int64_t ldp,
+                     const goat_options *opts, goat_fw_result *res);
+int goat_fw_core_csr_device(goat_handle *h, int64_t n, const goat_csr *dA, const goat_csr *dB,
+                            const void *dL, int64_t ldl, const void *dP0, int64_t ldp,
+                            const goat_options *opts, goat_fw_result *res);
+/* gradient on CSR adjacency, dense host P -> dense host G (float64). */
+int goat_gradient_csr(goat_handle *h, int64_t n, const goat_csr *A, const goat_csr *B,
+                      const double *P, int64_t ldp, double *G, int64_t ldg);
+/* timing hook: mean ms of `reps` CSR gradients on device CSR + dense device X (n x n). */
+int goat_bench_gradient_csr(goat_handle *h, int64_t n, const goat_csr *dA, const goat_csr *dB,
+                            const void *dX, int32_t reps, double *ms);
+
 /* matcher.py:100-107  G = A P B^T + A^T P B  (host float64 in/out). */
 int goat_gradient(goat_handle *h, int64_t n, const double *A, int64_t lda,
                   const double *B, int64_t ldb, const double *P, int64_t ldp,

@@ -48,6 +48,11 @@ class GoatFwResult(ctypes.Structure):
                 ("objective", ctypes.c_double), ("time_ms", ctypes.c_double * 6)]
 
 
+class GoatCsr(ctypes.Structure):
+    _fields_ = [("rowptr", _c_i64_p), ("colidx", _c_i32_p), ("values", ctypes.c_void_p),
+                ("nnz", ctypes.c_int64)]
+
+
 _lib = None
 _lib_lock = threading.Lock()
 
@@ -69,6 +74,18 @@ def _bind(lib):
                                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                                ctypes.POINTER(GoatOptions),
                                                ctypes.POINTER(GoatFwResult)]),
+        "goat_fw_core_csr": (ctypes.c_int, [H, ctypes.c_int64, ctypes.POINTER(GoatCsr), ctypes.POINTER(GoatCsr),
+                                            _c_double_p, ctypes.c_int64, _c_double_p, ctypes.c_int64,
+                                            ctypes.POINTER(GoatOptions), ctypes.POINTER(GoatFwResult)]),
+        "goat_fw_core_csr_device": (ctypes.c_int, [H, ctypes.c_int64, ctypes.POINTER(GoatCsr),
+                                                   ctypes.POINTER(GoatCsr), ctypes.c_void_p, ctypes.c_int64,
+                                                   ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(GoatOptions),
+                                                   ctypes.POINTER(GoatFwResult)]),
+        "goat_gradient_csr": (ctypes.c_int, [H, ctypes.c_int64, ctypes.POINTER(GoatCsr), ctypes.POINTER(GoatCsr),
+                                             _c_double_p, ctypes.c_int64, _c_double_p, ctypes.c_int64]),
+        "goat_bench_gradient_csr": (ctypes.c_int, [H, ctypes.c_int64, ctypes.POINTER(GoatCsr),
+                                                   ctypes.POINTER(GoatCsr), ctypes.c_void_p, ctypes.c_int32,
+                                                   _c_double_p]),
         "goat_gradient": (ctypes.c_int, [H, ctypes.c_int64, _c_double_p, ctypes.c_int64, _c_double_p,
                                          ctypes.c_int64, _c_double_p, ctypes.c_int64, _c_double_p,
                                          ctypes.c_int64]),
@@ -124,7 +141,8 @@ def _bind(lib):
 
 #: Every symbol include/goat.h declares (checked by tests/test_abi.py).
 EXPORTS = ("goat_create", "goat_destroy", "goat_last_error", "goat_version", "goat_reserve",
-           "goat_fw_core", "goat_fw_core_device", "goat_gradient", "goat_lot",
+           "goat_fw_core", "goat_fw_core_device", "goat_fw_core_csr", "goat_fw_core_csr_device",
+           "goat_gradient_csr", "goat_bench_gradient_csr", "goat_gradient", "goat_lot",
            "goat_sinkhorn_knopp", "goat_line_search_coeffs", "goat_lap",
            "goat_qap_objective_perm", "goat_set_stream", "goat_bench_sweep",
            "goat_bench_gradient", "goat_lap_device", "goat_shard_setup", "goat_shard_gradient",
@@ -224,3 +242,25 @@ def f64(a) -> np.ndarray:
 
 def ld_of(a: np.ndarray) -> int:
     return a.strides[0] // 8 if a.shape[0] > 1 else max(1, a.shape[1])
+
+
+def csr_struct(indptr, indices, values=None):
+    """goat_csr over numpy arrays (kept alive by the caller): int64 rowptr, int32
+    column indices, optional float64 values (None = every stored entry is 1)."""
+    c = GoatCsr()
+    c.rowptr = indptr.ctypes.data_as(_c_i64_p)
+    c.colidx = indices.ctypes.data_as(_c_i32_p)
+    c.values = ctypes.c_void_p(values.ctypes.data) if values is not None else None
+    c.nnz = int(indices.size)
+    return c
+
+
+def csr_struct_device(indptr, indices, values=None):
+    """goat_csr over torch CUDA tensors (rowptr int64, colidx int32, values of the
+    handle's element type or None)."""
+    c = GoatCsr()
+    c.rowptr = ctypes.cast(ctypes.c_void_p(indptr.data_ptr()), _c_i64_p)
+    c.colidx = ctypes.cast(ctypes.c_void_p(indices.data_ptr()), _c_i32_p)
+    c.values = ctypes.c_void_p(values.data_ptr()) if values is not None else None
+    c.nnz = int(indices.numel())
+    return c

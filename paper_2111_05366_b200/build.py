@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libgoat.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-SOURCES = ["goat_api.cu", "sinkhorn.cu", "reduce.cu", "gemm_simt.cu", "gemm_tc.cu", "lap.cu"]
+SOURCES = ["goat_api.cu", "sinkhorn.cu", "reduce.cu", "gemm_simt.cu", "gemm_tc.cu", "lap.cu", "spmm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC, "--expt-relaxed-constexpr"]

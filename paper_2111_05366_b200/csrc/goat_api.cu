@@ -59,6 +59,15 @@ struct Handle {
         SkPlan plan;
         DevBuf bad;               // per-column repair flags of the current sweep
     } sh;
+    // sparse (CSR) adjacency: A, A^T, B, B^T (goat_fw_core_csr*); values null = 0/1
+    struct Csr {
+        DevBuf rowptr, col, val;
+        int64_t nnz = 0;
+        bool has_val = false;
+    } csA, csAT, csB, csBT;
+    DevBuf csScratch;
+    bool csr_sym = false;
+    int64_t cap_ab = 0;  // dense A, B sized for this order
     double *h_scal = nullptr;                   // pinned host scalars
     int lap_stats[4] = {0, 0, 0, 0};            // last auction: assigned, rounds, capped, freed
     SkState *h_state = nullptr;                 // pinned
@@ -80,14 +89,19 @@ constexpr int kAuctionMinN = 256;
 
 // matrices = false: vectors, reduction scratch and LAP state only (the row-sharded
 // primitives keep their own blocks; a full n x n buffer per rank would defeat sharding).
-void ensure_workspace(Handle &h, int64_t n, bool matrices = true) {
+// dense = false: the CSR path, which never holds A or B as n x n matrices.
+void ensure_workspace(Handle &h, int64_t n, bool matrices = true, bool dense = true) {
     GOAT_CUDA(cudaSetDevice(h.device));
     const int64_t ld = ld_for(n);
     const size_t es = h.precision == GOAT_FP32 ? 4 : 8;
     const size_t mat = (size_t)n * ld * es;
     if (matrices && n > h.cap_mat) {
-        for (DevBuf *b : {&h.A, &h.B, &h.P, &h.Q, &h.G, &h.GQ, &h.T1, &h.M}) b->ensure(mat);
+        for (DevBuf *b : {&h.P, &h.Q, &h.G, &h.GQ, &h.T1, &h.M}) b->ensure(mat);
         h.cap_mat = n;
+    }
+    if (matrices && dense && n > h.cap_ab) {
+        for (DevBuf *b : {&h.A, &h.B}) b->ensure(mat);
+        h.cap_ab = n;
     }
     if (n <= h.cap_n) return;
     const size_t vec = (size_t)ld * 8;
@@ -124,6 +138,7 @@ struct Ctx {
     cudaStream_t s;
     bool sym = false;
     bool tc = false;  // gradient on tcgen05 (fp32 mode)
+    bool csr = false; // gradient by SpMM on the handle's CSR adjacency
     Ctx(Handle &hh, int nn) : h(hh), n(nn), ld(ld_for(nn)), s(hh.stream) {}
 };
 
@@ -286,10 +301,43 @@ void sync(Ctx &c) { GOAT_CUDA(cudaStreamSynchronize(c.s)); }
 
 // ------------------------------------------------------------------ gradient
 // out = A X B^T + A^T X B (matcher.py:107); symmetric inputs: 2 A X B.
+template <class T> DevCsr<T> csr_view(const Handle::Csr &m) {
+    DevCsr<T> v;
+    v.rowptr = m.rowptr.as<int64_t>();
+    v.col = m.col.as<int>();
+    v.val = m.has_val ? m.val.as<T>() : nullptr;
+    v.nnz = m.nnz;
+    return v;
+}
+
+// CSR gradient (spmm.cu): X1^T = (A X)^T [, X2^T = (A^T X)^T], then
+// out = (B X1^T [+ B^T X2^T])^T = A X B^T + A^T X B; symmetric: 2 (B X1^T)^T.
+template <class T> void csr_gradient(Ctx &c, const T *X, T *out, T *tmp) {
+    Handle &h = c.h;
+    const DevCsr<T> a = csr_view<T>(h.csA), at = csr_view<T>(h.csAT);
+    const DevCsr<T> b = csr_view<T>(h.csB), bt = csr_view<T>(h.csBT);
+    T *x1t = tmp, *x2t = h.M.as<T>();
+    const T *d1[1] = {X};
+    launch_spmm_t<T>(c.n, c.ld, 1, &a, d1, 1.0, x1t, c.s);
+    if (c.sym) {
+        const T *d2[1] = {x1t};
+        launch_spmm_t<T>(c.n, c.ld, 1, &b, d2, 2.0, out, c.s);
+    } else {
+        launch_spmm_t<T>(c.n, c.ld, 1, &at, d1, 1.0, x2t, c.s);
+        const DevCsr<T> s2[2] = {b, bt};
+        const T *d2[2] = {x1t, x2t};
+        launch_spmm_t<T>(c.n, c.ld, 2, s2, d2, 1.0, out, c.s);
+    }
+}
+
 template <class T>
 void gradient(Ctx &c, const T *A, const T *B, const T *X, T *out, T *tmp) {
     const int n = c.n;
     const int64_t ld = c.ld;
+    if (c.csr) {
+        csr_gradient<T>(c, X, out, tmp);
+        return;
+    }
     if constexpr (std::is_same<T, float>::value) {
         if (c.tc) {
             tc_gradient(c, X, out);
@@ -527,13 +575,27 @@ void fw_loop(Ctx &c, bool have_L, bool p0_bary, const goat_options &o, goat_fw_r
     double *hd = h.h_scal + 16;
     double t_grad = 0, t_lot = 0, t_ls = 0, t_lap = 0;
 
-    c.sym = is_symmetric<T>(c, A) && is_symmetric<T>(c, B);
-    setup_gemm<T>(c, A, B);
+    if (c.csr) {
+        c.sym = h.csr_sym;
+    } else {
+        c.sym = is_symmetric<T>(c, A) && is_symmetric<T>(c, B);
+        setup_gemm<T>(c, A, B);
+    }
     {
         Timer tm(c.s);
         if (p0_bary) {
             launch_fill<T>(P, ld, n, 1.0 / n, c.s);  // core.py:89-93
-            launch_bary_grad<T>(A, ld, B, ld, G, ld, n, h.vec.as<double>(), c.s);
+            if (c.csr) {
+                // degree vectors [A 1 | A^T 1 | B 1 | B^T 1] straight from the CSR rows
+                double *v = h.vec.as<double>();
+                launch_csr_rowsum<T>(csr_view<T>(h.csA), n, v, c.s);
+                launch_csr_rowsum<T>(csr_view<T>(h.csAT), n, v + n, c.s);
+                launch_csr_rowsum<T>(csr_view<T>(h.csB), n, v + 2 * n, c.s);
+                launch_csr_rowsum<T>(csr_view<T>(h.csBT), n, v + 3 * n, c.s);
+                launch_bary_grad_vec<T>(v, G, ld, n, c.s);
+            } else {
+                launch_bary_grad<T>(A, ld, B, ld, G, ld, n, h.vec.as<double>(), c.s);
+            }
         } else {
             gradient<T>(c, A, B, P, G, T1);
         }
@@ -802,6 +864,111 @@ template <class T> void shard_gradient(Handle &h, const T *Q, T *out) {
         gemm_simt<T>(m, n, n, 1.0, AT, ld, 0, Q, ld, 0, 0.0, X, ld, s);   // A^T_r Q
         gemm_simt<T>(m, n, n, 1.0, X, ld, 0, B, ld, 0, 1.0, out, ld, s);  // + (A^T_r Q) B
     }
+}
+
+
+// ------------------------------------------------------------------ CSR adjacency
+// Copies one CSR graph to the handle (host or device source; host values are
+// float64 and converted to the handle's precision), checks it (sorted rows,
+// columns in range, finite values), and builds its transpose.
+template <class T>
+void csr_load(Handle &h, int n, const goat_csr &src, bool device_src, Handle::Csr &dst, Handle::Csr &dstT,
+              cudaStream_t s) {
+    const int64_t nnz = src.nnz;
+    require(nnz >= 0 && src.rowptr && (nnz == 0 || src.colidx), "csr: NULL rowptr/colidx");
+    const auto kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (Handle::Csr *m : {&dst, &dstT}) {
+        m->rowptr.ensure((size_t)(n + 1) * 8);
+        m->col.ensure((size_t)std::max<int64_t>(nnz, 1) * 4);
+        m->nnz = nnz;
+        m->has_val = src.values != nullptr;
+        if (m->has_val) m->val.ensure((size_t)std::max<int64_t>(nnz, 1) * sizeof(T));
+    }
+    if (!device_src) {
+        require(src.rowptr[0] == 0 && src.rowptr[n] == nnz, "csr: rowptr[0] must be 0 and rowptr[n] = nnz");
+    }
+    GOAT_CUDA(cudaMemcpyAsync(dst.rowptr.p, src.rowptr, (size_t)(n + 1) * 8, kind, s));
+    if (nnz) GOAT_CUDA(cudaMemcpyAsync(dst.col.p, src.colidx, (size_t)nnz * 4, kind, s));
+    if (dst.has_val && nnz) {
+        if (device_src || sizeof(T) == 8) {
+            GOAT_CUDA(cudaMemcpyAsync(dst.val.p, src.values, (size_t)nnz * sizeof(T), kind, s));
+        } else {
+            std::vector<T> tmp((size_t)nnz);
+            const double *v = static_cast<const double *>(src.values);
+            for (int64_t q = 0; q < nnz; ++q) tmp[q] = (T)v[q];
+            GOAT_CUDA(cudaMemcpyAsync(dst.val.p, tmp.data(), (size_t)nnz * sizeof(T), cudaMemcpyHostToDevice, s));
+            GOAT_CUDA(cudaStreamSynchronize(s));  // tmp goes out of scope
+        }
+    }
+    int *flag = h.ivec.as<int>();
+    const int one = 1;
+    GOAT_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+    launch_csr_check<T>(csr_view<T>(dst), n, flag, s);
+    int ok = 0;
+    GOAT_CUDA(cudaMemcpyAsync(&ok, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GOAT_CUDA(cudaStreamSynchronize(s));
+    require(ok == 1, "csr: rows must hold strictly increasing column indices in [0, n) and finite values");
+    const size_t need = csr_transpose_scratch(nnz);
+    h.csScratch.ensure(need);
+    launch_csr_transpose<T>(csr_view<T>(dst), n, dstT.rowptr.as<int64_t>(), dstT.col.as<int>(),
+                            dstT.has_val ? dstT.val.as<T>() : nullptr, h.csScratch.p, h.csScratch.bytes, s);
+}
+
+template <class T> bool csr_equal(Handle &h, int n, const Handle::Csr &a, const Handle::Csr &b, cudaStream_t s) {
+    int *flag = h.ivec.as<int>();
+    const int one = 1;
+    GOAT_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+    launch_csr_equal<T>(csr_view<T>(a), csr_view<T>(b), n, flag, s);
+    int r = 0;
+    GOAT_CUDA(cudaMemcpyAsync(&r, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GOAT_CUDA(cudaStreamSynchronize(s));
+    return r == 1;
+}
+
+template <class T> void csr_setup(Handle &h, int n, const goat_csr &A, const goat_csr &B, bool device_src) {
+    ensure_workspace(h, n, true, false);
+    cudaStream_t s = h.stream;
+    csr_load<T>(h, n, A, device_src, h.csA, h.csAT, s);
+    csr_load<T>(h, n, B, device_src, h.csB, h.csBT, s);
+    h.csr_sym = csr_equal<T>(h, n, h.csA, h.csAT, s) && csr_equal<T>(h, n, h.csB, h.csBT, s);
+    // SpMM writes only columns [0, n) of each row: keep the padding of every n x n buffer zero
+    for (DevBuf *b : {&h.P, &h.Q, &h.G, &h.GQ, &h.T1, &h.M}) GOAT_CUDA(cudaMemsetAsync(b->p, 0, b->bytes, s));
+}
+
+template <class T>
+void fw_core_csr(Handle &h, int64_t n, const goat_csr &A, const goat_csr &B, bool device_src, const void *L,
+                 int64_t ldl, const void *P0, int64_t ldp, const goat_options *o, goat_fw_result *res) {
+    auto t0 = std::chrono::steady_clock::now();
+    Ctx c(h, (int)n);
+    Timer setup(c.s);
+    csr_setup<T>(h, (int)n, A, B, device_src);
+    c.csr = true;
+    const size_t es = sizeof(T);
+    if (L) { h.L.ensure(h.P.bytes); h.Gl.ensure(h.P.bytes); GOAT_CUDA(cudaMemsetAsync(h.L.p, 0, h.L.bytes, c.s)); }
+    if (device_src) {
+        auto cp = [&](const void *src, int64_t lds, T *dst) {
+            GOAT_CUDA(cudaMemcpy2DAsync(dst, c.ld * es, src, lds * es, n * es, n, cudaMemcpyDeviceToDevice, c.s));
+        };
+        if (L) cp(L, ldl, h.L.as<T>());
+        if (P0) cp(P0, ldp, h.P.as<T>());
+    } else if (L || P0) {
+        h.stage.ensure((size_t)n * c.ld * 8);
+        if (L) upload<T>(c, static_cast<const double *>(L), ldl, h.L.as<T>(), h.stage.as<double>());
+        if (P0) upload<T>(c, static_cast<const double *>(P0), ldp, h.P.as<T>(), h.stage.as<double>());
+    }
+    res->time_ms[4] = setup.stop();
+    fw_loop<T>(c, L != nullptr, P0 == nullptr, *o, res);
+    // objective on the inputs (core.py:120-124): sum over A's entries of A_ij B_{p(i)p(j)}
+    int *perm = h.ivec.as<int>();
+    std::vector<int> ph(n);
+    for (int64_t r = 0; r < n; ++r) ph[r] = (int)res->assignment[r];
+    GOAT_CUDA(cudaMemcpyAsync(perm, ph.data(), n * 4, cudaMemcpyHostToDevice, c.s));
+    launch_csr_qap_perm<T>(csr_view<T>(h.csA), csr_view<T>(h.csB), perm, (int)n, h.vec.as<double>(),
+                           h.scal.as<double>() + 40, c.s);
+    GOAT_CUDA(cudaMemcpyAsync(h.h_scal + 40, h.scal.as<double>() + 40, 8, cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    res->objective = h.h_scal[40];
+    res->time_ms[5] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
 template <class T> SkArgs shard_sk_args(Handle &h, const void *G) {
@@ -1454,6 +1621,83 @@ int goat_lap_device(goat_handle *h, int64_t n, const void *dM, int64_t ldm, int3
                 sync(c);
                 *objective = h->h_scal[56];
             }
+        });
+    });
+}
+
+
+int goat_fw_core_csr(goat_handle *h, int64_t n, const goat_csr *A, const goat_csr *B, const double *L, int64_t ldl,
+                     const double *P0, int64_t ldp, const goat_options *opts, goat_fw_result *res) {
+    return guarded([&] {
+        require(h && A && B && res && res->assignment && res->hist_obj && res->hist_alpha, "NULL argument");
+        check_order(n);
+        validate_opts(opts);
+        require((!L || ldl >= n) && (!P0 || ldp >= n), "leading dimension < n");
+        launch_count() = 0;
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            fw_core_csr<T>(*h, n, *A, *B, false, L, ldl, P0, ldp, opts, res);
+        });
+        res->gpu_launches = (int32_t)launch_count();
+    });
+}
+
+int goat_fw_core_csr_device(goat_handle *h, int64_t n, const goat_csr *dA, const goat_csr *dB, const void *dL,
+                            int64_t ldl, const void *dP0, int64_t ldp, const goat_options *opts,
+                            goat_fw_result *res) {
+    return guarded([&] {
+        require(h && dA && dB && res && res->assignment && res->hist_obj && res->hist_alpha, "NULL argument");
+        check_order(n);
+        validate_opts(opts);
+        require((!dL || ldl >= n) && (!dP0 || ldp >= n), "leading dimension < n");
+        launch_count() = 0;
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            fw_core_csr<T>(*h, n, *dA, *dB, true, dL, ldl, dP0, ldp, opts, res);
+        });
+        res->gpu_launches = (int32_t)launch_count();
+    });
+}
+
+int goat_gradient_csr(goat_handle *h, int64_t n, const goat_csr *A, const goat_csr *B, const double *P, int64_t ldp,
+                      double *G, int64_t ldg) {
+    return guarded([&] {
+        require(h && A && B && P && G, "NULL argument");
+        check_order(n);
+        require(ldp >= n && ldg >= n, "leading dimension < n");
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            csr_setup<T>(*h, (int)n, *A, *B, false);
+            h->stage.ensure((size_t)n * ld_for(n) * 8);
+            Ctx c(*h, (int)n);
+            c.csr = true;
+            c.sym = h->csr_sym;
+            double *stage = h->stage.as<double>();
+            upload<T>(c, P, ldp, h->P.as<T>(), stage);
+            gradient<T>(c, (const T *)nullptr, (const T *)nullptr, h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());
+            download<T>(c, h->G.as<T>(), G, ldg, stage);
+        });
+    });
+}
+
+int goat_bench_gradient_csr(goat_handle *h, int64_t n, const goat_csr *dA, const goat_csr *dB, const void *dX,
+                            int32_t reps, double *ms) {
+    return guarded([&] {
+        require(h && dA && dB && dX && ms && reps >= 1, "NULL argument");
+        check_order(n);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            csr_setup<T>(*h, (int)n, *dA, *dB, true);
+            Ctx c(*h, (int)n);
+            c.csr = true;
+            c.sym = h->csr_sym;
+            const size_t es = sizeof(T);
+            GOAT_CUDA(cudaMemcpy2DAsync(h->P.p, c.ld * es, dX, n * es, n * es, n, cudaMemcpyDeviceToDevice, c.s));
+            gradient<T>(c, (const T *)nullptr, (const T *)nullptr, h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());
+            Timer tm(c.s);
+            for (int r = 0; r < reps; ++r)
+                gradient<T>(c, (const T *)nullptr, (const T *)nullptr, h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());
+            *ms = tm.stop() / reps;
         });
     });
 }

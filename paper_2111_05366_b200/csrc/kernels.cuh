@@ -115,6 +115,33 @@ void launch_is_symmetric(const T *X, int64_t ld, int n, int *flag, cudaStream_t 
 template <class T>
 void launch_neglog(const T *X, int64_t ldx, T *Y, int64_t ldy, int n, int *bad, cudaStream_t s);
 
+// G_ij = (ra_i rb_j + ca_i cb_j) / n from the four degree vectors (vec4n = [ra|ca|rb|cb])
+template <class T> void launch_bary_grad_vec(const double *vec4n, T *G, int64_t ldg, int n, cudaStream_t s);
+
+// ---------------------------------------------------------------- sparse (CSR) adjacency (spmm.cu)
+template <class T> struct DevCsr {
+    const int64_t *rowptr = nullptr;  // [n+1]
+    const int *col = nullptr;         // [nnz], strictly increasing within a row
+    const T *val = nullptr;           // [nnz] or null: every stored entry is 1
+    int64_t nnz = 0;
+};
+// out = alpha * (sum_t S_t D_t)^T, t < nterms (1 or 2); D_t, out: n x ld row-major
+template <class T>
+void launch_spmm_t(int n, int64_t ld, int nterms, const DevCsr<T> *S, const T *const *D, double alpha, T *out,
+                   cudaStream_t s);
+// flag[0] <- 0 unless every row is strictly increasing, in range, and values are finite
+template <class T> void launch_csr_check(const DevCsr<T> &a, int n, int *flag, cudaStream_t s);
+size_t csr_transpose_scratch(int64_t nnz);
+template <class T>
+void launch_csr_transpose(const DevCsr<T> &a, int n, int64_t *rowptrT, int *colT, T *valT, void *scratch,
+                          size_t scratch_bytes, cudaStream_t s);
+template <class T> void launch_csr_equal(const DevCsr<T> &a, const DevCsr<T> &b, int n, int *flag, cudaStream_t s);
+template <class T> void launch_csr_rowsum(const DevCsr<T> &a, int n, double *rs, cudaStream_t s);
+// out[0] = sum_{(i,j) in A} A_ij B_{p(i) p(j)}  (fp64, fixed order; rowsum: n doubles of scratch)
+template <class T>
+void launch_csr_qap_perm(const DevCsr<T> &a, const DevCsr<T> &b, const int *perm, int n, double *rowsum, double *out,
+                         cudaStream_t s);
+
 // ---------------------------------------------------------------- GEMM
 // C = alpha * op(A) op(B) + beta * C, op = transpose when trans != 0 (SIMT).
 template <class T>

@@ -282,6 +282,13 @@ void launch_bary_grad(const T *A, int64_t lda, const T *B, int64_t ldb, T *G, in
     GOAT_CHECK_LAUNCH();
 }
 
+template <class T> void launch_bary_grad_vec(const double *vec4n, T *G, int64_t ldg, int n, cudaStream_t s) {
+    bary_grad_kernel<T><<<std::min(n, 4096), kThreads, 0, s>>>(vec4n, vec4n + n, vec4n + 2 * n, vec4n + 3 * n, G,
+                                                                 ldg, n);
+    note_launch();
+    GOAT_CHECK_LAUNCH();
+}
+
 template <class T> void launch_is_symmetric(const T *X, int64_t ld, int n, int *flag, cudaStream_t s) {
     symmetric_kernel<T><<<std::min(n, 4096), kThreads, 0, s>>>(X, ld, n, flag); note_launch();
     GOAT_CHECK_LAUNCH();
@@ -306,6 +313,7 @@ void launch_neglog(const T *X, int64_t ldx, T *Y, int64_t ldy, int n, int *bad, 
     template void launch_bary_grad<T>(const T *, int64_t, const T *, int64_t, T *, int64_t, int,     \
                                       double *, cudaStream_t);                                       \
     template void launch_is_symmetric<T>(const T *, int64_t, int, int *, cudaStream_t);              \
+    template void launch_bary_grad_vec<T>(const double *, T *, int64_t, int, cudaStream_t);          \
     template void launch_neglog<T>(const T *, int64_t, T *, int64_t, int, int *, cudaStream_t);
 GOAT_INST(float)
 GOAT_INST(double)

@@ -13,6 +13,7 @@ LOT, exact line search, update, final LAP) runs on the device in one
 
 from __future__ import annotations
 
+import ctypes
 import time
 
 import numpy as np
@@ -22,7 +23,7 @@ from .matrices import as_square_matrix, invert_permutation, permute_matrix, qap_
 from .ops import randomized_blend_init
 from .records import MatchOptions, MatchResult, SeedSet
 
-__all__ = ["frank_wolfe_match", "seeded_match", "fw_core"]
+__all__ = ["frank_wolfe_match", "seeded_match", "fw_core", "fw_core_csr", "as_csr", "is_sparse"]
 
 
 def fw_core(A, B, L, P0, opts: MatchOptions):
@@ -37,6 +38,13 @@ def fw_core(A, B, L, P0, opts: MatchOptions):
     B_ = _lib.f64(B)
     L_ = _lib.f64(L) if L is not None else None
     P_ = _lib.f64(P0) if P0 is not None else None
+    return _call_core(n, opts, h, lambda lib, o, res: lib.goat_fw_core(
+        h.ptr, n, _lib.dptr(A_), _lib.ld_of(A_), _lib.dptr(B_), _lib.ld_of(B_),
+        _lib.dptr(L_) if L_ is not None else None, _lib.ld_of(L_) if L_ is not None else n,
+        _lib.dptr(P_) if P_ is not None else None, _lib.ld_of(P_) if P_ is not None else n, o, res))
+
+
+def _call_core(n, opts: MatchOptions, h, call):
     mi = opts.max_iters
     assign = np.empty(n, dtype=np.int64)
     hobj = np.empty(mi + 1)
@@ -58,11 +66,7 @@ def fw_core(A, B, L, P0, opts: MatchOptions):
         fw_tol=opts.fw_tol, lam=opts.sinkhorn.lam, sk_tol=opts.sinkhorn.tol)
     lib = _lib.load()
     with h.lock:
-        _lib.check(lib.goat_fw_core(
-            h.ptr, n, _lib.dptr(A_), _lib.ld_of(A_), _lib.dptr(B_), _lib.ld_of(B_),
-            _lib.dptr(L_) if L_ is not None else None, _lib.ld_of(L_) if L_ is not None else n,
-            _lib.dptr(P_) if P_ is not None else None, _lib.ld_of(P_) if P_ is not None else n,
-            o, res))
+        _lib.check(call(lib, ctypes.byref(o), ctypes.byref(res)))
     it = int(res.iterations)
     history = [(0, float(hobj[0]), None)]
     history += [(i, float(hobj[i]), float(halpha[i])) for i in range(1, it + 1)]
@@ -72,6 +76,59 @@ def fw_core(A, B, L, P0, opts: MatchOptions):
                 time_ms=dict(zip(("gradient", "lot", "line_search", "lap", "setup", "total"),
                                  list(res.time_ms))))
     return assign.astype(np.intp), history, it, bool(res.converged), diag
+
+
+def is_sparse(M) -> bool:
+    """scipy.sparse matrices and CSR graphs (graphs.CsrGraph) take the CSR path."""
+    from .graphs import CsrGraph
+    try:
+        import scipy.sparse as sp
+        if sp.issparse(M):
+            return True
+    except ImportError:  # pragma: no cover
+        pass
+    return isinstance(M, CsrGraph)
+
+
+def as_csr(M, name: str = "matrix"):
+    """Canonical float64 scipy CSR (sorted rows, duplicates summed) with the
+    reference's validation (core.py:17-27): square, finite."""
+    import scipy.sparse as sp
+
+    from .graphs import CsrGraph
+    if isinstance(M, CsrGraph):
+        M = sp.csr_matrix((np.ones(M.indices.size), M.indices, M.indptr), shape=(M.n, M.n))
+    M = sp.csr_matrix(M, dtype=np.float64)
+    if M.ndim != 2 or M.shape[0] != M.shape[1]:
+        raise ValueError(f"{name} must be square, got shape {M.shape}")
+    M.sum_duplicates()
+    M.sort_indices()
+    if not np.all(np.isfinite(M.data)):
+        raise ValueError(f"{name} contains non-finite entries")
+    return M
+
+
+def _csr_arrays(M):
+    indptr = np.ascontiguousarray(M.indptr, dtype=np.int64)
+    indices = np.ascontiguousarray(M.indices, dtype=np.int32)
+    vals = None if np.all(M.data == 1.0) else np.ascontiguousarray(M.data, dtype=np.float64)
+    return indptr, indices, vals
+
+
+def fw_core_csr(A, B, L, P0, opts: MatchOptions):
+    """``fw_core`` for CSR adjacency (gradient by SpMM; goat_fw_core_csr)."""
+    A = as_csr(A, "A")
+    B = as_csr(B, "B")
+    n = A.shape[0]
+    h = _lib.handle(opts.device, opts.precision)
+    aa, ba = _csr_arrays(A), _csr_arrays(B)
+    ca, cb = _lib.csr_struct(*aa), _lib.csr_struct(*ba)
+    L_ = _lib.f64(L) if L is not None else None
+    P_ = _lib.f64(P0) if P0 is not None else None
+    return _call_core(n, opts, h, lambda lib, o, res: lib.goat_fw_core_csr(
+        h.ptr, n, ctypes.byref(ca), ctypes.byref(cb),
+        _lib.dptr(L_) if L_ is not None else None, _lib.ld_of(L_) if L_ is not None else n,
+        _lib.dptr(P_) if P_ is not None else None, _lib.ld_of(P_) if P_ is not None else n, o, res))
 
 
 def _initial(n, opts: MatchOptions, rng):
@@ -93,8 +150,15 @@ def _quadratic_1x1(A22, B22, L):
 
 def _match(A, B, pairs: np.ndarray, opts: MatchOptions) -> MatchResult:
     t0 = time.perf_counter()
-    A = as_square_matrix(A, "A")
-    B = as_square_matrix(B, "B")
+    sparse = is_sparse(A) or is_sparse(B)
+    if sparse:
+        # CSR path: the same host bookkeeping on scipy CSR matrices; the core
+        # runs goat_fw_core_csr (SpMM gradient, no dense A or B on the device)
+        A = as_csr(A, "A")
+        B = as_csr(B, "B")
+    else:
+        A = as_square_matrix(A, "A")
+        B = as_square_matrix(B, "B")
     if A.shape != B.shape:
         raise ValueError(f"order mismatch: {A.shape[0]} vs {B.shape[0]}")
     n = A.shape[0]
@@ -108,8 +172,12 @@ def _match(A, B, pairs: np.ndarray, opts: MatchOptions) -> MatchResult:
     rest2 = np.setdiff1d(np.arange(n), pairs[:, 1]) if m else np.arange(n)
     ord1 = np.concatenate([pairs[:, 0], rest1]).astype(np.intp)
     ord2 = np.concatenate([pairs[:, 1], rest2]).astype(np.intp)
-    Ar = A[np.ix_(ord1, ord1)] if m else A
-    Br = B[np.ix_(ord2, ord2)] if m else B
+    if sparse:
+        Ar = A[ord1][:, ord1] if m else A
+        Br = B[ord2][:, ord2] if m else B
+    else:
+        Ar = A[np.ix_(ord1, ord1)] if m else A
+        Br = B[np.ix_(ord2, ord2)] if m else B
     nf = n - m
     best = None
     for r in range(opts.n_restarts):
@@ -119,20 +187,26 @@ def _match(A, B, pairs: np.ndarray, opts: MatchOptions) -> MatchResult:
         else:
             shuf = np.arange(nf, dtype=np.intp)
         inv = invert_permutation(shuf)
-        B22 = permute_matrix(Br[m:, m:], shuf) if opts.shuffle_input else Br[m:, m:]
+        if sparse:
+            B22 = Br[m:, m:][inv][:, inv] if opts.shuffle_input else Br[m:, m:]
+        else:
+            B22 = permute_matrix(Br[m:, m:], shuf) if opts.shuffle_input else Br[m:, m:]
         A22 = Ar[m:, m:]
         L = None
         if m:
             B12 = Br[:m, m:][:, inv]
             B21 = Br[m:, :m][inv, :]
             L = Ar[m:, :m] @ B21.T + Ar[:m, m:].T @ B12  # constant seed term (matcher.py:267)
+            if sparse:
+                L = np.asarray(L.toarray(), dtype=np.float64)
         diag = None
         if nf == 1:
             p22 = np.zeros(1, dtype=np.intp)
             history, iters, conv = [(0, _quadratic_1x1(A22, B22, L), None)], 0, True
         else:
             P0 = _initial(nf, opts, rng)
-            p22, history, iters, conv, diag = fw_core(A22, B22, L, P0, opts)
+            core = fw_core_csr if sparse else fw_core
+            p22, history, iters, conv, diag = core(A22, B22, L, P0, opts)
         p22 = inv[p22]
         align = np.empty(n, dtype=np.intp)
         align[ord1[:m]] = ord2[:m]
@@ -140,6 +214,8 @@ def _match(A, B, pairs: np.ndarray, opts: MatchOptions) -> MatchResult:
         if m == 0 and diag is not None:
             # same terms A_ij B_{align(i) align(j)}, already reduced on the device
             obj = diag["objective"]
+        elif sparse:
+            obj = float(A.multiply(B[align][:, align]).sum())  # core.py:120-124 on the CSR inputs
         else:
             obj = qap_objective(A, B, align, device=opts.device)
         if best is None or (obj > best[1] if opts.objective_sense == "maximize" else obj < best[1]):

@@ -82,3 +82,21 @@ def test_product_path_fails_loudly_without_gpu():
     A = np.zeros((4, 4))
     with pytest.raises(RuntimeError):
         gb.frank_wolfe_match(A, A, gb.MatchOptions(step_solver="lot"))
+
+
+def test_as_csr_validation_and_canonical_form():
+    import scipy.sparse as sp
+
+    from paper_2111_05366_b200 import engine, graphs
+    M = sp.coo_matrix((np.array([1.0, 2.0, 3.0]), (np.array([0, 0, 1]), np.array([2, 2, 0]))), shape=(3, 3))
+    C = engine.as_csr(M)
+    assert C.has_sorted_indices and C.nnz == 2 and C[0, 2] == 3.0  # duplicates summed
+    with pytest.raises(ValueError):
+        engine.as_csr(sp.csr_matrix(np.ones((2, 3))))
+    with pytest.raises(ValueError):
+        engine.as_csr(sp.csr_matrix(np.array([[0.0, np.inf], [1.0, 0.0]])))
+    A, B, truth = graphs.config_pair(5, 0, n=300)
+    assert engine.is_sparse(A) and not engine.is_sparse(A.to_dense())
+    np.testing.assert_array_equal(engine.as_csr(A).toarray(), A.to_dense())
+    ip, ix, v = engine._csr_arrays(engine.as_csr(A))
+    assert v is None and ip.dtype == np.int64 and ix.dtype == np.int32
