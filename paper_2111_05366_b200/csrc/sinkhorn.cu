@@ -1260,7 +1260,6 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
     }
     // lagged state (clusters): the previous band's exponentials and warp max
     constexpr bool LAGGED = CL > 1;
-    T yp[CH][VW];
     T mp = neg_inf<T>();
     double devmax = 0.0;  // pre-check only (writer thread)
     __shared__ T s_wp[2][NW][2];
@@ -1277,7 +1276,8 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
         const unsigned b = b0 + (unsigned)it;
         // keep S - 1 bands in flight beyond the one being loaded (never blocks in
         // steady state: every warp passed the block barrier of band b - 1)
-        if (tid == 0) pipe_produce<NW, CL>(a, sl, rg, ps, b + (unsigned)S - 1);
+        // (clusters: a stage is released only after its lagged finish, one band later)
+        if (tid == 0) pipe_produce<NW, CL>(a, sl, rg, ps, b + (unsigned)S - (LAGGED ? 2u : 1u));
         T y[CH][VW];
         T m = neg_inf<T>();
         if (it < nrows) {
@@ -1292,8 +1292,10 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
                 else xv = make_float4(0.f, 0.f, 0.f, 0.f);
                 y[c][0] = xv.x; y[c][1] = xv.y; y[c][2] = xv.z; y[c][3] = xv.w;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ps.empty[s]);
+            if constexpr (!LAGGED) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ps.empty[s]);
+            }
             if constexpr (MAXP) {
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
@@ -1331,6 +1333,16 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
                     sp[e] += v;
                 }
             T sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+            if constexpr (LAGGED) {
+                // the exponentials wait in the stage for the lagged finish (registers
+                // stay free for one band: no spills at 128 registers/thread)
+                V *stw = reinterpret_cast<V *>(rg.base + (size_t)s * rg.stage_bytes);
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const int col = c0 + (tid + NT * c) * VW;
+                    if (col < c1 && !rowonly) stw[tid + NT * c] = make_float4(y[c][0], y[c][1], y[c][2], y[c][3]);
+                }
+            }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
             if (lane == 0) { s_wp[b & 1][warp][0] = m; s_wp[b & 1][warp][1] = sum; }
@@ -1391,12 +1403,20 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
                     for (int q = 0; q < CL; ++q) Sm += sq[q];
                     bad |= !(Sm >= kShiftLo && Sm <= kShiftHi);
                 }
-                PIPE_FINISH(it - 1, (double)M + SkMath<T>::lgt(Sm), mp, yp);
+                const int sf = (int)(bf % (unsigned)S);
+                const V *stf = reinterpret_cast<const V *>(rg.base + (size_t)sf * rg.stage_bytes);
+                T yl[CH][VW];
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const int col = c0 + (tid + NT * c) * VW;
+                    const V yv = (col < c1 && !rowonly) ? stf[tid + NT * c] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    yl[c][0] = yv.x; yl[c][1] = yv.y; yl[c][2] = yv.z; yl[c][3] = yv.w;
+                }
+                fence_proxy_async_smem();  // this thread's stage accesses precede the bulk refill
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ps.empty[sf]);
+                PIPE_FINISH(it - 1, (double)M + SkMath<T>::lgt(Sm), mp, yl);
             }
-#pragma unroll
-            for (int c = 0; c < CH; ++c)
-#pragma unroll
-                for (int e = 0; e < VW; ++e) yp[LAGGED ? c : 0][e] = y[c][e];
             mp = m;
         }
     }
@@ -1909,12 +1929,20 @@ bool pipe_plan(int n, int mrows, SkPlan &p) {
     p.slice_w = (int)round_up(n, 8 * VW);
     p.ch = std::max(3, ceil_div(ceil_div(n, VW), p.nt));
     if (p.ch > env_int("GOAT_SK_PIPE_CH1", 6)) {
-        // Clustered pipeline: correct, but measured slower than the lock-step
-        // cluster kernel (sk_persistent_kernel, TMA ring) at n = 16384-65536 --
-        // the lagged band needs two exponential sets in registers and spills.
-        // Opt in with GOAT_SK_PIPE=2 (profiles/round1_sk_pipe.md).
-        if (env_int("GOAT_SK_PIPE", 1) != 2) return false;
-        const int maxch = std::min(6, env_int("GOAT_SK_PIPE_CH", 5));
+        // Clustered rows: the pipelined kernel keeps a band's exponentials in its
+        // stage until the lagged cluster finish.  It measured faster than the
+        // lock-step cluster kernel where both split rows the same way with <= 6
+        // chunks per thread (n = 20000: 0.487 vs 0.521 ms, n = 40000: 2.155 vs
+        // 2.339 ms); where the lock-step kernel can hold 7-8 chunks per thread
+        // instead (n = 16384 unsplit, n = 65536 in 4 slices) it keeps the bigger
+        // bands and wins (profiles/round1_sk_pipe.md).  GOAT_SK_PIPE=2 forces it.
+        int lcl = 1, lch = ceil_div(ceil_div(n, VW), kWideThreads);
+        while (lch > kMaxCh && lcl < 8) {
+            lcl *= 2;
+            lch = ceil_div(ceil_div((int)round_up(ceil_div(n, lcl), 8 * VW), VW), kWideThreads);
+        }
+        if (env_int("GOAT_SK_PIPE", 1) != 2 && (lcl == 1 || lch > 6)) return false;
+        const int maxch = std::min(6, env_int("GOAT_SK_PIPE_CH", 6));
         while (p.cl < 8) {
             p.cl *= 2;
             p.slice_w = (int)round_up(ceil_div(n, p.cl), 8 * VW);

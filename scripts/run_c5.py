@@ -2,7 +2,9 @@
 device path (goat_fw_core_device) for a few outer iterations, phase split,
 per-iteration LOT sweeps, and the match ratio against the hidden permutation.
 
-usage: python scripts/run_c5.py [max_iters] [n] [fp32|fp64] [auto|simt]
+usage: python scripts/run_c5.py [max_iters] [n] [fp32|fp64] [csr|auto|simt]
+(csr = goat_fw_core_csr_device, the SpMM gradient on the CSR graphs; the other
+modes densify A and B and run goat_fw_core_device)
 """
 import ctypes
 import json
@@ -20,7 +22,7 @@ iters = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 n_arg = int(sys.argv[2]) if len(sys.argv) > 2 else None
 prec = sys.argv[3] if len(sys.argv) > 3 else "fp32"
 tdt = torch.float32 if prec == "fp32" else torch.float64
-gemm = sys.argv[4] if len(sys.argv) > 4 else "auto"
+gemm = sys.argv[4] if len(sys.argv) > 4 else "csr"
 t0 = time.perf_counter()
 A, Bs, truth = graphs.config_pair(5, 0, n=n_arg)
 n = A.n
@@ -35,9 +37,13 @@ def dense(g):
     return d
 
 
-dA, dB = dense(A), dense(Bs)
+if gemm != "csr":
+    dA, dB = dense(A), dense(Bs)
+else:
+    csr_t = [torch.from_numpy(x).to(dev) for x in (A.indptr, A.indices, Bs.indptr, Bs.indices)]
+    sA, sB = _lib.csr_struct_device(csr_t[0], csr_t[1]), _lib.csr_struct_device(csr_t[2], csr_t[3])
 torch.cuda.synchronize()
-h = _lib.handle(0, prec, gemm)
+h = _lib.handle(0, prec, "auto" if gemm == "csr" else gemm)
 lib = _lib.load()
 _lib.check(lib.goat_set_stream(h.ptr, _lib.stream_handle(torch.cuda.current_stream(dev))))
 assign = np.empty(n, dtype=np.int64)
@@ -51,8 +57,12 @@ res.lot_converged = lconv.ctypes.data_as(_lib._c_i32_p)
 o = _lib.GoatOptions(max_iters=iters, max_sweeps=1000, sense=_lib.GOAT_MAXIMIZE, step_solver=_lib.GOAT_STEP_LOT,
                      fw_tol=1e-2, lam=100.0, sk_tol=1e-8)
 t1 = time.perf_counter()
-_lib.check(lib.goat_fw_core_device(h.ptr, n, ctypes.c_void_p(dA.data_ptr()), n, ctypes.c_void_p(dB.data_ptr()), n,
-                                   None, n, None, n, o, res))
+if gemm == "csr":
+    _lib.check(lib.goat_fw_core_csr_device(h.ptr, n, ctypes.byref(sA), ctypes.byref(sB), None, n, None, n,
+                                           ctypes.byref(o), ctypes.byref(res)))
+else:
+    _lib.check(lib.goat_fw_core_device(h.ptr, n, ctypes.c_void_p(dA.data_ptr()), n, ctypes.c_void_p(dB.data_ptr()),
+                                       n, None, n, None, n, o, res))
 wall = time.perf_counter() - t1
 it = res.iterations
 inv = np.empty(n, dtype=np.int64)
