@@ -348,6 +348,177 @@ __global__ void lap_auction_unlink(int n, const int *col4row, int *row4col) {
     }
 }
 
+
+// ------------------------------------------------------------------ cluster repair
+// Warm-started augmenting paths for large n on a thread-block cluster.  The
+// single-CTA solver above keeps all per-column state in global memory once n
+// outgrows shared memory, so every Dijkstra step streams ~25 bytes per column
+// through one SM.  Here CL CTAs split the columns into contiguous slices held in
+// shared memory (spc, v, path, row4col, and ucol = u of the row matched to the
+// column), each step reads only its slice of the cost row, and the step's argmin
+// is a candidate exchange through distributed shared memory plus one cluster
+// barrier.  Ties: smallest reduced cost, then a free column, then the lowest
+// index (deterministic).  Dual updates and the augmentation are the same as the
+// single-CTA solver, so the result is an exact optimum (scipy's, up to ties).
+struct LapCand {
+    double v;      // reduced cost
+    double unext;  // u of the row matched to column j
+    int j;         // column (INT_MAX: none)
+    int inext;     // row matched to j (-1: free)
+    int free;
+    int pad;
+};
+
+__device__ __forceinline__ bool cand_less(const LapCand &a, const LapCand &b) {
+    if (a.v != b.v) return a.v < b.v;
+    if (a.free != b.free) return a.free > b.free;
+    return a.j < b.j;
+}
+
+__device__ __forceinline__ unsigned cl_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <class P> __device__ __forceinline__ P *cl_map(P *p, unsigned rank) {
+    // generic address of the same shared-memory object in CTA `rank`
+    void *r;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(p), "r"(rank));
+    return static_cast<P *>(r);
+}
+
+constexpr int kLapClThreads = 1024;
+
+template <class T, int CL>
+__global__ void __launch_bounds__(kLapClThreads, 1)
+    lap_cluster_sap_kernel(const T *M, int64_t ld, int n, double sign, LapWork w, int W) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double *spc = reinterpret_cast<double *>(smem);
+    double *v = spc + W;
+    double *ucol = v + W;
+    int *path = reinterpret_cast<int *>(ucol + W);
+    int *r4c = path + W;
+    unsigned char *SC = reinterpret_cast<unsigned char *>(r4c + W);
+    __shared__ LapCand cand[2][CL];
+    __shared__ LapCand s_warp[kLapClThreads / 32];
+    const unsigned rank = cl_rank();
+    const int c0 = (int)rank * W, c1 = min(n, c0 + W);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int *col4row = w.col4row;
+    for (int j = c0 + tid; j < c1; j += kLapClThreads) {
+        const int jl = j - c0;
+        v[jl] = w.v[j];
+        const int r = w.row4col[j];
+        r4c[jl] = r;
+        ucol[jl] = r >= 0 ? w.u[r] : 0.0;
+    }
+    cl_sync();
+    int par = 0;
+    for (int cur = 0; cur < n; ++cur) {
+        if (__ldcg(col4row + cur) != -1) continue;  // matched (uniform: published by the last cluster barrier)
+        for (int j = c0 + tid; j < c1; j += kLapClThreads) { SC[j - c0] = 0; spc[j - c0] = INFINITY; }
+        __syncthreads();
+        const double ucur = __ldcg(w.u + cur);
+        double minv = 0.0, ui = ucur;
+        int i = cur, sink = -1;
+        for (;;) {
+            const T *Mi = M + (int64_t)i * ld;
+            LapCand b{INFINITY, 0.0, INT_MAX, -1, 0, 0};
+            for (int j = c0 + tid; j < c1; j += kLapClThreads) {
+                const int jl = j - c0;
+                if (SC[jl]) continue;
+                const double r = ((minv + sign * (double)Mi[j]) - ui) - v[jl];
+                double sj = spc[jl];
+                if (r < sj) { path[jl] = i; spc[jl] = r; sj = r; }
+                const LapCand c{sj, 0.0, j, 0, r4c[jl] == -1 ? 1 : 0, 0};
+                if (cand_less(c, b)) b = c;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                LapCand o;
+                o.v = __shfl_xor_sync(0xffffffffu, b.v, off);
+                o.j = __shfl_xor_sync(0xffffffffu, b.j, off);
+                o.free = __shfl_xor_sync(0xffffffffu, b.free, off);
+                if (cand_less(o, b)) b = o;
+            }
+            if (lane == 0) s_warp[warp] = b;
+            __syncthreads();
+            if (warp == 0) {
+                LapCand c = s_warp[lane];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    LapCand o;
+                    o.v = __shfl_xor_sync(0xffffffffu, c.v, off);
+                    o.j = __shfl_xor_sync(0xffffffffu, c.j, off);
+                    o.free = __shfl_xor_sync(0xffffffffu, c.free, off);
+                    if (cand_less(o, c)) c = o;
+                }
+                if (c.j != INT_MAX) {
+                    c.inext = r4c[c.j - c0];
+                    c.unext = ucol[c.j - c0];
+                }
+                // this CTA's candidate into slot [par][rank] of every CTA of the cluster
+                if (lane < CL) *cl_map(&cand[par][rank], (unsigned)lane) = c;
+            }
+            cl_sync();
+            LapCand g = cand[par][0];
+#pragma unroll
+            for (int q = 1; q < CL; ++q)
+                if (cand_less(cand[par][q], g)) g = cand[par][q];
+            par ^= 1;
+            if (!(g.v < INFINITY)) {
+                if (rank == 0 && tid == 0) *w.status = -1;
+                return;  // uniform across the cluster
+            }
+            // the thread that scans column g.j marks it (no barrier before its next read)
+            if (g.j >= c0 && g.j < c1 && (g.j - c0) % kLapClThreads == tid) SC[g.j - c0] = 1;
+            minv = g.v;
+            if (g.free) { sink = g.j; break; }
+            i = g.inext;
+            ui = g.unext;
+        }
+        __syncthreads();
+        // dual update (matcher order of the single-CTA solver): scanned columns
+        for (int j = c0 + tid; j < c1; j += kLapClThreads) {
+            const int jl = j - c0;
+            if (!SC[jl]) continue;
+            const double d = minv - spc[jl];
+            v[jl] -= d;
+            if (j != sink) ucol[jl] += d;  // u of the visited row matched to j
+        }
+        cl_sync();
+        if (rank == 0 && tid == 0) {
+            // augment along the path: sink <- ... <- cur (ucol moves with its row)
+            const double unew = ucur + minv;
+            int j = sink;
+            for (;;) {
+                const unsigned oj = (unsigned)(j / W);
+                const int r = *cl_map(&path[j - (int)oj * W], oj);
+                const int t = __ldcg(col4row + r);
+                double ur = unew;
+                if (r != cur) {
+                    const unsigned ot = (unsigned)(t / W);
+                    ur = *cl_map(&ucol[t - (int)ot * W], ot);
+                }
+                *cl_map(&r4c[j - (int)oj * W], oj) = r;
+                *cl_map(&ucol[j - (int)oj * W], oj) = ur;
+                col4row[r] = j;
+                if (r == cur) break;
+                j = t;
+            }
+        }
+        cl_sync();
+    }
+    for (int j = c0 + tid; j < c1; j += kLapClThreads) {
+        w.row4col[j] = r4c[j - c0];
+        w.v[j] = v[j - c0];
+    }
+    if (rank == 0 && tid == 0) *w.status = 0;
+}
+
 }  // namespace
 
 template <class T>
@@ -392,9 +563,49 @@ void launch_lap_certificate(const T *M, int64_t ld, int n, int sense, int *cand,
     GOAT_CHECK_LAUNCH();
 }
 
+template <class T, int CL>
+bool try_cluster_sap(const T *M, int64_t ld, int n, double sign, const LapWork &w, cudaStream_t s) {
+    const int W = (int)round_up(ceil_div(n, CL), 8);
+    const size_t smem = (size_t)W * (8 + 8 + 8 + 4 + 4 + 1) + 16;
+    if (smem > 200 * 1024) return false;
+    auto fn = lap_cluster_sap_kernel<T, CL>;
+    GOAT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (CL > 8) GOAT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(kLapClThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    GOAT_CUDA(cudaLaunchKernelEx(&cfg, fn, M, ld, n, sign, w, W));
+    note_launch();
+    return true;
+}
+
 template <class T>
 void launch_lap_sap(const T *M, int64_t ld, int n, int sense, const LapWork &w, cudaStream_t s, int warm) {
     const size_t smem = (size_t)n * (8 + 8 + 4 + 4 + 4 + 1) + 16;
+    const char *lce = getenv("GOAT_LAP_CLUSTER");  // 0: never, 2: always (tests), else when smem overflows
+    const int lc = lce ? atoi(lce) : 1;
+    if (warm && lc != 0 && (smem > 200 * 1024 || lc == 2)) {
+        // warm repair too large for one CTA's shared memory: the cluster solver
+        const double sign = (sense == GOAT_MAXIMIZE) ? -1.0 : 1.0;
+        if (try_cluster_sap<T, 16>(M, ld, n, sign, w, s) || try_cluster_sap<T, 8>(M, ld, n, sign, w, s)) {
+            GOAT_CHECK_LAUNCH();
+            return;
+        }
+    }
     int use_smem = smem <= 200 * 1024;
     if (use_smem)
         GOAT_CUDA(cudaFuncSetAttribute(lap_sap_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

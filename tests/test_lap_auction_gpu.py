@@ -36,3 +36,20 @@ def test_auction_lap_matches_scipy(n, kind, sense):
             # (seen on the fp32-rounded hub matrix): same objective, valid bijection
             gb.as_permutation(sol.assignment)
             assert Mp[np.arange(n), sol.assignment].sum() == Mp[np.arange(n), pp].sum()
+
+
+@pytest.mark.parametrize("n", [700, 3000])
+@pytest.mark.parametrize("kind", ["uniform", "hub"])
+@pytest.mark.parametrize("sense", ["maximize", "minimize"])
+def test_cluster_repair_matches_scipy(n, kind, sense, monkeypatch):
+    """The cluster-split augmenting-path repair (used once the single-CTA state
+    outgrows shared memory, n >~ 7000) forced at smaller n: scipy's optimum."""
+    monkeypatch.setenv("GOAT_LAP_CLUSTER", "2")
+    rng = np.random.default_rng(7 * n + (kind == "hub"))
+    M = rng.random((n, n)) if kind == "uniform" else _hub(n, rng)
+    p, v = O.lap(M, sense)
+    sol = gb.solve_lap(M, sense, precision="fp64")
+    assert sol.objective == v
+    gb.as_permutation(sol.assignment)
+    if not np.array_equal(sol.assignment, p):
+        assert M[np.arange(n), sol.assignment].sum() == M[np.arange(n), p].sum()
