@@ -212,3 +212,44 @@ def config_pair(config, replicate=0, n=None):
         raise ValueError(c["kind"])
     Bs, truth = shuffle(B, rng)
     return A, Bs, truth
+
+
+def sparse_er_pair_csr_device(n, p, rho, seed=0, device="cuda", block_rows=2048):
+    """Config-5 law (undirected correlated sparse ER, samplers.py:60-65 conditional
+    law, hollow, mirrored) drawn on the GPU with torch's generator -- the bench's
+    fast stand-in for ``sparse_er_pair_csr`` (same law, different random stream).
+
+    Returns ((rowptr_A, col_A), (rowptr_B, col_B), truth) as CUDA tensors (int64
+    rowptr, int32 columns, rows sorted) with B relabelled by the hidden permutation.
+    """
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(int(seed))
+    ra, ca, rb, cb = [], [], [], []
+    cols = torch.arange(n, device=device)
+    for r0 in range(0, n, block_rows):
+        r1 = min(n, r0 + block_rows)
+        U = torch.rand((r1 - r0, n), generator=g, device=device)
+        V = torch.rand((r1 - r0, n), generator=g, device=device)
+        upper = cols[None, :] > torch.arange(r0, r1, device=device)[:, None]
+        a = (U < p) & upper
+        b = torch.where(U < p, V < p + rho * (1.0 - p), V < p * (1.0 - rho)) & upper
+        i, j = torch.nonzero(a, as_tuple=True)
+        ra.append(i + r0); ca.append(j)
+        i, j = torch.nonzero(b, as_tuple=True)
+        rb.append(i + r0); cb.append(j)
+        del U, V, a, b, upper
+    perm = torch.randperm(n, generator=g, device=device)
+
+    def csr(r, c, relabel=None):
+        r = torch.cat(r); c = torch.cat(c)
+        r, c = torch.cat([r, c]), torch.cat([c, r])
+        if relabel is not None:
+            r, c = relabel[r], relabel[c]
+        key, _ = torch.sort(r * n + c)
+        r, c = key // n, (key % n).to(torch.int32)
+        rowptr = torch.zeros(n + 1, dtype=torch.int64, device=device)
+        rowptr[1:] = torch.cumsum(torch.bincount(r, minlength=n), 0)
+        return rowptr, c.contiguous()
+
+    return csr(ra, ca), csr(rb, cb, perm), perm
