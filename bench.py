@@ -390,7 +390,7 @@ def _kernel_scan(lib, h, dev, hbm_peak):
         out[f"sinkhorn_sweep_n{n}"] = {"us": ms * 1e3, "GB_s": gbs, "frac_hbm": gbs / hbm_peak,
                                        "bytes": n * n * 4}
         del G
-    for n, sym in ((2000, False), (5000, True)):
+    for n, sym in ((2000, False), (5000, True), (8192, True)):
         g = torch.Generator(device=dev).manual_seed(n)
         A = (torch.rand((n, n), device=dev, generator=g) < 0.3).float()
         B = (torch.rand((n, n), device=dev, generator=g) < 0.3).float()

@@ -1200,7 +1200,7 @@ __device__ __forceinline__ void pipe_produce(const SkArgs &a, const Slice &sl, P
 // the row's LSE, no max reduction is needed, and the pairs reduce to plain sums.
 // A row whose sum leaves [2^-40, 2^100] (early sweeps: g moved by > 40 log2
 // units) sets the redo flag and the whole sweep is recomputed with MAXP.
-constexpr int kPipeShiftRows = 4096;
+constexpr int kPipeShiftRows = 2048;
 constexpr float kShiftLo = 9.094947e-13f;   // 2^-40
 constexpr float kShiftHi = 1.2676506e30f;   // 2^100
 
@@ -1909,11 +1909,14 @@ void *pipe_for(int ch, int cl, int nt) {
             case 4: return pipe_fn<4, C>();               \
             case 5: return pipe_fn<5, C>();               \
             case 6: return pipe_fn<6, C>();               \
+            case 7: return pipe_fn<7, C>();               \
         }                                                 \
     }
     GOAT_PCL(1)
     GOAT_PCL(2)
+    GOAT_PCL(3)
     GOAT_PCL(4)
+    GOAT_PCL(6)
     GOAT_PCL(8)
 #undef GOAT_PCL
     throw Error(GOAT_ENOTSUP, "sinkhorn: no pipelined kernel for chunks=" + std::to_string(ch) + " cluster=" +
@@ -1942,21 +1945,30 @@ bool pipe_plan(int n, int mrows, SkPlan &p) {
             lch = ceil_div(ceil_div((int)round_up(ceil_div(n, lcl), 8 * VW), VW), kWideThreads);
         }
         if (env_int("GOAT_SK_PIPE", 1) != 2 && (lcl == 1 || lch > 6)) return false;
-        const int maxch = std::min(6, env_int("GOAT_SK_PIPE_CH", 6));
-        while (p.cl < 8) {
-            p.cl *= 2;
-            p.slice_w = (int)round_up(ceil_div(n, p.cl), 8 * VW);
-            p.ch = std::max(3, ceil_div(ceil_div(p.slice_w, VW), p.nt));
-            if (p.ch <= maxch) break;
+        // the same split as the lock-step kernel, unless GOAT_SK_PIPE_CL forces one
+        // (3- and 6-CTA clusters measured slower: fewer co-resident SMs).  The
+        // lagged finish holds two stages, so at least four must fit beside g.
+        const int maxch = std::min(7, env_int("GOAT_SK_PIPE_CH", 7));
+        const int force = env_int("GOAT_SK_PIPE_CL", 0);
+        bool found = false;
+        for (int cl : {2, 3, 4, 6, 8}) {
+            if (force ? cl != force : (cl != lcl && env_int("GOAT_SK_PIPE", 1) != 2) || cl == 3 || cl == 6) continue;
+            const int sw = (int)round_up(ceil_div(n, cl), 8 * VW);
+            const int ch = std::max(3, ceil_div(ceil_div(sw, VW), p.nt));
+            const size_t stage = round_up((size_t)sw * sizeof(float), 128), glb = (size_t)p.nt * ch * 16;
+            if (ch > maxch || (220 * 1024 - glb) / stage < 4) continue;
+            p.cl = cl; p.slice_w = sw; p.ch = ch;
+            found = true;
+            break;
         }
-        if (p.ch > 6) return false;
+        if (!found) return false;
     }
     p.rows = 1;
     p.pipe = true;
     // ring stages + one more slice for g (scaled), within ~216 KB of dynamic smem
     p.stage_bytes = (int)round_up((size_t)p.slice_w * sizeof(float), 128);
     const size_t gl_bytes = (size_t)p.nt * p.ch * 16;  // every thread's chunks, masked ones included
-    p.stages = std::min(8, (int)((216 * 1024 - gl_bytes) / p.stage_bytes));
+    p.stages = std::min(8, (int)((220 * 1024 - gl_bytes) / p.stage_bytes));
     if (const int st = env_int("GOAT_SK_STAGES", 0)) p.stages = std::min(p.stages, std::max(3, st));
     if (p.stages < 3) return false;
     p.smem = (size_t)p.stages * p.stage_bytes + gl_bytes;
