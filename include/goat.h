@@ -205,6 +205,12 @@ int goat_lap_device(goat_handle *h, int64_t n, const void *dM, int64_t ldm, int3
 int goat_shard_setup(goat_handle *h, int64_t n, int64_t m, const void *dA_rows, const void *dAT_rows,
                      const void *dB, int64_t ld);
 /* G_r = (A_r Q) B^T + (A^T_r Q) B from the gathered Q (n x ld). */
+/* Row-sharded setup on CSR adjacency (device pointers, values of the handle's
+ * element type or NULL): this rank's m rows of A and of A^T (global column
+ * indices; rowptr[0] = 0), and the whole B and B^T.  A^T rows and B^T are NULL
+ * together for symmetric inputs.  The gradient then runs as SpMMs. */
+int goat_shard_setup_csr(goat_handle *h, int64_t n, int64_t m, const goat_csr *dA_rows,
+                         const goat_csr *dAT_rows, const goat_csr *dB, const goat_csr *dBT);
 int goat_shard_gradient(goat_handle *h, const void *dQ_full, void *dOut_rows);
 /* local (min, max) of a block (the LOT scale is global: min/max-allreduce). */
 int goat_shard_minmax(goat_handle *h, const void *dX_rows, double *out2);

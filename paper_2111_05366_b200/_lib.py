@@ -116,6 +116,9 @@ def _bind(lib):
         "goat_shard_setup": (ctypes.c_int, [H, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                             ctypes.c_void_p, ctypes.c_int64]),
         "goat_shard_gradient": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_void_p]),
+        "goat_shard_setup_csr": (ctypes.c_int, [H, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(GoatCsr),
+                                                ctypes.POINTER(GoatCsr), ctypes.POINTER(GoatCsr),
+                                                ctypes.POINTER(GoatCsr)]),
         "goat_shard_minmax": (ctypes.c_int, [H, ctypes.c_void_p, _c_double_p]),
         "goat_shard_lot_begin": (ctypes.c_int, [H, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
                                                 ctypes.c_double, ctypes.c_int32, ctypes.c_double]),
@@ -145,7 +148,7 @@ EXPORTS = ("goat_create", "goat_destroy", "goat_last_error", "goat_version", "go
            "goat_gradient_csr", "goat_bench_gradient_csr", "goat_gradient", "goat_lot",
            "goat_sinkhorn_knopp", "goat_line_search_coeffs", "goat_lap",
            "goat_qap_objective_perm", "goat_set_stream", "goat_bench_sweep",
-           "goat_bench_gradient", "goat_lap_device", "goat_shard_setup", "goat_shard_gradient",
+           "goat_bench_gradient", "goat_lap_device", "goat_shard_setup", "goat_shard_setup_csr", "goat_shard_gradient",
            "goat_shard_minmax", "goat_shard_lot_begin", "goat_shard_lot_pass", "goat_shard_lot_merge",
            "goat_shard_lot_status", "goat_shard_lot_repair_pass", "goat_shard_lot_repair_merge",
            "goat_shard_lot_emit", "goat_shard_dots", "goat_shard_axpby",

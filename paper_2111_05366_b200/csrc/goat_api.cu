@@ -58,6 +58,7 @@ struct Handle {
         int na = 0, nb = 0;
         SkPlan plan;
         DevBuf bad;               // per-column repair flags of the current sweep
+        bool csr = false;         // gradient by SpMM on CSR rows (goat_shard_setup_csr)
     } sh;
     // sparse (CSR) adjacency: A, A^T, B, B^T (goat_fw_core_csr*); values null = 0/1
     struct Csr {
@@ -65,6 +66,7 @@ struct Handle {
         int64_t nnz = 0;
         bool has_val = false;
     } csA, csAT, csB, csBT;
+    Csr shA, shAT, shB, shBT;  // row-sharded CSR: this rank's rows of A, A^T; B, B^T
     DevBuf csScratch;
     bool csr_sym = false;
     int64_t cap_ab = 0;  // dense A, B sized for this order
@@ -318,15 +320,15 @@ template <class T> void csr_gradient(Ctx &c, const T *X, T *out, T *tmp) {
     const DevCsr<T> b = csr_view<T>(h.csB), bt = csr_view<T>(h.csBT);
     T *x1t = tmp, *x2t = h.M.as<T>();
     const T *d1[1] = {X};
-    launch_spmm_t<T>(c.n, c.ld, 1, &a, d1, 1.0, x1t, c.s);
+    launch_spmm_t<T>(c.n, c.n, c.ld, c.ld, 1, &a, d1, 1.0, x1t, c.s);
     if (c.sym) {
         const T *d2[1] = {x1t};
-        launch_spmm_t<T>(c.n, c.ld, 1, &b, d2, 2.0, out, c.s);
+        launch_spmm_t<T>(c.n, c.n, c.ld, c.ld, 1, &b, d2, 2.0, out, c.s);
     } else {
-        launch_spmm_t<T>(c.n, c.ld, 1, &at, d1, 1.0, x2t, c.s);
+        launch_spmm_t<T>(c.n, c.n, c.ld, c.ld, 1, &at, d1, 1.0, x2t, c.s);
         const DevCsr<T> s2[2] = {b, bt};
         const T *d2[2] = {x1t, x2t};
-        launch_spmm_t<T>(c.n, c.ld, 2, s2, d2, 1.0, out, c.s);
+        launch_spmm_t<T>(c.n, c.n, c.ld, c.ld, 2, s2, d2, 1.0, out, c.s);
     }
 }
 
@@ -825,11 +827,33 @@ void shard_tc_prepare(Handle &h) {
     if (!S.sym) tc_split_planes_t(B, ld, n, pb + mat, ld, bstride, S.nb, s);
 }
 
+template <class T> DevCsr<T> csr_view(const Handle::Csr &m);
+
 template <class T> void shard_gradient(Handle &h, const T *Q, T *out) {
     auto &S = h.sh;
     const int n = (int)S.n, m = (int)S.m;
     const int64_t ld = ld_for(n), mat = (int64_t)n * ld;
     cudaStream_t s = h.stream;
+    if (S.csr) {
+        // X1^T = (A_r Q)^T [, X2^T = (A^T_r Q)^T]  (n x m), then
+        // G_r = (B X1^T [+ B^T X2^T])^T  (m x n) = A_r Q B^T + A^T_r Q B
+        const int64_t ldm = ld_for(m);
+        T *x1t = S.X.as<T>(), *x2t = x1t + (int64_t)n * ldm;
+        const DevCsr<T> a = csr_view<T>(h.shA), at = csr_view<T>(h.shAT);
+        const DevCsr<T> b = csr_view<T>(h.shB), bt = csr_view<T>(h.shBT);
+        const T *d1[1] = {Q};
+        launch_spmm_t<T>(m, n, ld, ldm, 1, &a, d1, 1.0, x1t, s);
+        if (S.sym) {
+            const T *d2[1] = {x1t};
+            launch_spmm_t<T>(n, m, ldm, ld, 1, &b, d2, 2.0, out, s);
+        } else {
+            launch_spmm_t<T>(m, n, ld, ldm, 1, &at, d1, 1.0, x2t, s);
+            const DevCsr<T> s2[2] = {b, bt};
+            const T *d2[2] = {x1t, x2t};
+            launch_spmm_t<T>(n, m, ldm, ld, 2, s2, d2, 1.0, out, s);
+        }
+        return;
+    }
     if constexpr (std::is_same<T, float>::value) {
         if (S.tc) {
             const int SP = h.split;
@@ -903,7 +927,7 @@ void csr_load(Handle &h, int n, const goat_csr &src, bool device_src, Handle::Cs
     int *flag = h.ivec.as<int>();
     const int one = 1;
     GOAT_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, s));
-    launch_csr_check<T>(csr_view<T>(dst), n, flag, s);
+    launch_csr_check<T>(csr_view<T>(dst), n, n, flag, s);
     int ok = 0;
     GOAT_CUDA(cudaMemcpyAsync(&ok, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     GOAT_CUDA(cudaStreamSynchronize(s));
@@ -1387,7 +1411,7 @@ int goat_shard_setup(goat_handle *h, int64_t n, int64_t m, const void *dA_rows, 
         ensure_workspace(*h, n, false);
         auto &S = h->sh;
         S.ready = false;
-        S.n = n; S.m = m; S.sym = (dAT_rows == nullptr); S.fill = false;
+        S.n = n; S.m = m; S.sym = (dAT_rows == nullptr); S.fill = false; S.csr = false;
         const int64_t lw = ld_for(n);
         const size_t es = h->precision == GOAT_FP32 ? 4 : 8;
         cudaStream_t s = h->stream;
@@ -1402,6 +1426,61 @@ int goat_shard_setup(goat_handle *h, int64_t n, int64_t m, const void *dA_rows, 
         S.X.ensure((size_t)m * lw * es);
         S.tc = h->precision == GOAT_FP32 && h->gemm != GOAT_GEMM_SIMT;
         if (S.tc) shard_tc_prepare(*h);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            S.plan = sk_plan<T>((int)n, h->num_sms, (int)m);
+        });
+        h->colpart.ensure(S.plan.colpart_bytes);
+        S.bad.ensure((size_t)ld_for(n));
+        GOAT_CUDA(cudaStreamSynchronize(s));
+        S.ready = true;
+    });
+}
+
+int goat_shard_setup_csr(goat_handle *h, int64_t n, int64_t m, const goat_csr *dA_rows, const goat_csr *dAT_rows,
+                         const goat_csr *dB, const goat_csr *dBT) {
+    return guarded([&] {
+        require(h && dA_rows && dB && (!dAT_rows) == (!dBT), "NULL argument (A^T rows and B^T go together)");
+        check_order(n);
+        require(m >= 1 && m <= n, "block rows must be in [1, n]");
+        ensure_workspace(*h, n, false);
+        auto &S = h->sh;
+        S.ready = false;
+        S.n = n; S.m = m; S.sym = (dAT_rows == nullptr); S.fill = false; S.csr = true; S.tc = false;
+        const size_t es = h->precision == GOAT_FP32 ? 4 : 8;
+        cudaStream_t s = h->stream;
+        auto put = [&](Handle::Csr &dst, const goat_csr &src, int64_t rows) {
+            const int64_t nnz = src.nnz;
+            require(nnz >= 0 && src.rowptr && (nnz == 0 || src.colidx), "csr: NULL rowptr/colidx");
+            dst.rowptr.ensure((size_t)(rows + 1) * 8);
+            dst.col.ensure((size_t)std::max<int64_t>(nnz, 1) * 4);
+            dst.nnz = nnz;
+            dst.has_val = src.values != nullptr;
+            GOAT_CUDA(cudaMemcpyAsync(dst.rowptr.p, src.rowptr, (size_t)(rows + 1) * 8, cudaMemcpyDeviceToDevice, s));
+            if (nnz) GOAT_CUDA(cudaMemcpyAsync(dst.col.p, src.colidx, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, s));
+            if (dst.has_val) {
+                dst.val.ensure((size_t)std::max<int64_t>(nnz, 1) * es);
+                if (nnz) GOAT_CUDA(cudaMemcpyAsync(dst.val.p, src.values, (size_t)nnz * es, cudaMemcpyDeviceToDevice, s));
+            }
+            int *flag = h->ivec.as<int>();
+            const int one = 1;
+            GOAT_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+            dispatch(*h, [&](auto *tag) {
+                using T = std::remove_pointer_t<decltype(tag)>;
+                launch_csr_check<T>(csr_view<T>(dst), (int)rows, (int)n, flag, s);
+            });
+            int ok = 0;
+            GOAT_CUDA(cudaMemcpyAsync(&ok, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+            GOAT_CUDA(cudaStreamSynchronize(s));
+            require(ok == 1, "csr: rows must hold strictly increasing column indices in [0, n) and finite values");
+        };
+        put(h->shB, *dB, n);
+        if (!S.sym) put(h->shBT, *dBT, n);
+        put(h->shA, *dA_rows, m);  // m rows over n columns
+        if (!S.sym) put(h->shAT, *dAT_rows, m);
+        const int64_t ldm = ld_for(m);
+        S.X.ensure((size_t)2 * n * ldm * es);
+        GOAT_CUDA(cudaMemsetAsync(S.X.p, 0, S.X.bytes, s));
         dispatch(*h, [&](auto *tag) {
             using T = std::remove_pointer_t<decltype(tag)>;
             S.plan = sk_plan<T>((int)n, h->num_sms, (int)m);

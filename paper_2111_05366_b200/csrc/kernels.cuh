@@ -125,12 +125,15 @@ template <class T> struct DevCsr {
     const T *val = nullptr;           // [nnz] or null: every stored entry is 1
     int64_t nnz = 0;
 };
-// out = alpha * (sum_t S_t D_t)^T, t < nterms (1 or 2); D_t, out: n x ld row-major
+// out = alpha * (sum_t S_t D_t)^T, t < nterms (1 or 2).  S_t: `rows` CSR rows over
+// column indices < (rows of D_t); D_t: row-major with `cols` columns, leading dim
+// ld; out: cols x rows row-major, leading dim ldo (columns >= rows untouched).
 template <class T>
-void launch_spmm_t(int n, int64_t ld, int nterms, const DevCsr<T> *S, const T *const *D, double alpha, T *out,
-                   cudaStream_t s);
-// flag[0] <- 0 unless every row is strictly increasing, in range, and values are finite
-template <class T> void launch_csr_check(const DevCsr<T> &a, int n, int *flag, cudaStream_t s);
+void launch_spmm_t(int rows, int cols, int64_t ld, int64_t ldo, int nterms, const DevCsr<T> *S, const T *const *D,
+                   double alpha, T *out, cudaStream_t s);
+// flag[0] <- 0 unless rowptr spans [0, nnz], every row is strictly increasing with
+// columns in [0, n), and the values are finite
+template <class T> void launch_csr_check(const DevCsr<T> &a, int rows, int n, int *flag, cudaStream_t s);
 size_t csr_transpose_scratch(int64_t nnz);
 template <class T>
 void launch_csr_transpose(const DevCsr<T> &a, int n, int64_t *rowptrT, int *colT, T *valT, void *scratch,

@@ -1362,7 +1362,7 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) Sm += __shfl_xor_sync(0xffffffffu, Sm, off);
             if constexpr (!LAGGED) {
-                if constexpr (!MAXP) bad |= !(Sm >= kShiftLo && Sm <= kShiftHi);
+                if constexpr (!MAXP) bad |= !(Sm >= kShiftLo && Sm <= kShiftHi) || a.resident == 3;
                 PIPE_FINISH(it, (double)M + SkMath<T>::lgt(Sm), m, y);
             } else {
                 // this CTA's pair -> every rank of the cluster; finished next band
@@ -1401,7 +1401,7 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
                     M = mq[0];  // the common shift
 #pragma unroll
                     for (int q = 0; q < CL; ++q) Sm += sq[q];
-                    bad |= !(Sm >= kShiftLo && Sm <= kShiftHi);
+                    bad |= !(Sm >= kShiftLo && Sm <= kShiftHi) || a.resident == 3;
                 }
                 const int sf = (int)(bf % (unsigned)S);
                 const V *stf = reinterpret_cast<const V *>(rg.base + (size_t)sf * rg.stage_bytes);
@@ -1453,7 +1453,9 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
     }
 }
 
-__device__ __forceinline__ bool env_shift_ok(const SkArgs &a) { return a.resident != 2; }  // resident==2: force max
+// GOAT_SK_RES (SkArgs::resident): 2 = max shift only, 3 = flag every fixed-shift sweep
+// for a redo (tests of the redo path)
+__device__ __forceinline__ bool env_shift_ok(const SkArgs &a) { return a.resident != 2; }
 
 template <int CH, int CL, int NT>
 __global__ void __launch_bounds__(NT, 1) sk_pipe_kernel(SkArgs a, unsigned *bar) {

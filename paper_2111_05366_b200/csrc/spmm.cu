@@ -34,8 +34,10 @@ template <> struct SpVec<double> { using V = double2; static constexpr int W = 2
 
 template <class T, int NTERMS>
 struct SpmmArgs {
-    int n;
-    int64_t ld;
+    int rows;       // rows of every S_t (= columns of out)
+    int cols;       // columns of every D_t (= rows of out)
+    int64_t ld;     // leading dimension of D_t
+    int64_t ldo;    // leading dimension of out
     const int64_t *rowptr[2];
     const int *col[2];
     const T *val[2];
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(kSpThreads) spmm_t_kernel(SpmmArgs<T, NTERMS> 
     const int i0 = rt * kSpRows, j0 = cb * kSpCols;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int jl = j0 + lane * 8;
-    const bool jok = jl < p.n;  // ld >= round_up(n, 8): a started 8-chunk is in bounds
+    const bool jok = jl < p.cols;  // ld >= round_up(cols, 8): a started 8-chunk is in bounds
 #pragma unroll 1
     for (int r = 0; r < 4; ++r) {
         const int li = warp * 4 + r;
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(kSpThreads) spmm_t_kernel(SpmmArgs<T, NTERMS> 
         T acc[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[e] = T(0);
-        if (i < p.n) {
+        if (i < p.rows) {
 #pragma unroll
             for (int t = 0; t < NTERMS; ++t) {
                 const int64_t q0 = p.rowptr[t][i], q1 = p.rowptr[t][i + 1];
@@ -114,14 +116,15 @@ __global__ void __launch_bounds__(kSpThreads) spmm_t_kernel(SpmmArgs<T, NTERMS> 
     for (int c = warp; c < kSpCols; c += kSpThreads / 32) {
         const int j = j0 + c;
         const int i = i0 + lane;
-        if (j < p.n && i < p.n) p.out[(int64_t)j * p.ld + i] = alpha * tile[c * (kSpRows + 1) + lane];
+        if (j < p.cols && i < p.rows) p.out[(int64_t)j * p.ldo + i] = alpha * tile[c * (kSpRows + 1) + lane];
     }
 }
 
 // ---------------------------------------------------------------- CSR utilities
 // flag[0] <- 0 if some row is not strictly increasing or a column is out of range
-__global__ void csr_check_kernel(const int64_t *rowptr, const int *col, int n, int64_t nnz, int *flag) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+__global__ void csr_check_kernel(const int64_t *rowptr, const int *col, int rows, int n, int64_t nnz, int *flag) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (rowptr[0] != 0 || rowptr[rows] != nnz)) *flag = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
         const int64_t a = rowptr[i], b = rowptr[i + 1];
         if (a > b || a < 0 || b > nnz) { *flag = 0; continue; }
         int prev = -1;
@@ -236,15 +239,16 @@ __global__ void fixed_sum_kernel(const double *v, int n, double *out) {
 }  // namespace
 
 template <class T>
-void launch_spmm_t(int n, int64_t ld, int nterms, const DevCsr<T> *S, const T *const *D, double alpha, T *out,
-                   cudaStream_t s) {
+void launch_spmm_t(int rows, int cols, int64_t ld, int64_t ldo, int nterms, const DevCsr<T> *S, const T *const *D,
+                   double alpha, T *out, cudaStream_t s) {
     require(nterms == 1 || nterms == 2, "spmm: 1 or 2 terms");
-    const int nrt = ceil_div(n, kSpRows), ncb = ceil_div(n, kSpCols);
+    require(ld >= round_up(cols, 8) && ldo >= rows, "spmm: leading dimension");
+    const int nrt = ceil_div(rows, kSpRows), ncb = ceil_div(cols, kSpCols);
     const size_t smem = (size_t)kSpCols * (kSpRows + 1) * sizeof(T);
     const int64_t grid = (int64_t)nrt * ncb;
     require(grid < (1ll << 31), "spmm: order too large");
     auto fill = [&](auto &p) {
-        p.n = n; p.ld = ld; p.out = out; p.alpha = alpha; p.nrt = nrt;
+        p.rows = rows; p.cols = cols; p.ld = ld; p.ldo = ldo; p.out = out; p.alpha = alpha; p.nrt = nrt;
         for (int t = 0; t < nterms; ++t) {
             p.rowptr[t] = S[t].rowptr; p.col[t] = S[t].col; p.val[t] = S[t].val; p.D[t] = D[t];
         }
@@ -264,9 +268,9 @@ void launch_spmm_t(int n, int64_t ld, int nterms, const DevCsr<T> *S, const T *c
     GOAT_CHECK_LAUNCH();
 }
 
-template <class T> void launch_csr_check(const DevCsr<T> &a, int n, int *flag, cudaStream_t s) {
-    csr_check_kernel<<<std::max(1, std::min(ceil_div(n, kThreads), 1184)), kThreads, 0, s>>>(a.rowptr, a.col, n,
-                                                                                              a.nnz, flag);
+template <class T> void launch_csr_check(const DevCsr<T> &a, int rows, int n, int *flag, cudaStream_t s) {
+    csr_check_kernel<<<std::max(1, std::min(ceil_div(rows, kThreads), 1184)), kThreads, 0, s>>>(a.rowptr, a.col, rows,
+                                                                                                 n, a.nnz, flag);
     note_launch();
     if (a.val && a.nnz) {
         finite_kernel<T><<<1184, kThreads, 0, s>>>(a.val, a.nnz, flag);
@@ -340,9 +344,9 @@ void launch_csr_qap_perm(const DevCsr<T> &a, const DevCsr<T> &b, const int *perm
 }
 
 #define GOAT_SP_INST(T)                                                                                          \
-    template void launch_spmm_t<T>(int, int64_t, int, const DevCsr<T> *, const T *const *, double, T *,        \
-                                   cudaStream_t);                                                                \
-    template void launch_csr_check<T>(const DevCsr<T> &, int, int *, cudaStream_t);                              \
+    template void launch_spmm_t<T>(int, int, int64_t, int64_t, int, const DevCsr<T> *, const T *const *, double, \
+                                   T *, cudaStream_t);                                                           \
+    template void launch_csr_check<T>(const DevCsr<T> &, int, int, int *, cudaStream_t);                         \
     template void launch_csr_transpose<T>(const DevCsr<T> &, int, int64_t *, int *, T *, void *, size_t,        \
                                           cudaStream_t);                                                         \
     template void launch_csr_equal<T>(const DevCsr<T> &, const DevCsr<T> &, int, int *, cudaStream_t);          \

@@ -90,6 +90,11 @@ def is_sparse(M) -> bool:
     return isinstance(M, CsrGraph)
 
 
+def CsrGraphType():
+    from .graphs import CsrGraph
+    return CsrGraph
+
+
 def as_csr(M, name: str = "matrix"):
     """Canonical float64 scipy CSR (sorted rows, duplicates summed) with the
     reference's validation (core.py:17-27): square, finite."""

@@ -138,6 +138,15 @@ class GpuShardBackend:
                                              AT_rows.data_ptr() if AT_rows is not None else None,
                                              B.data_ptr(), L.ld))
 
+    def setup_csr(self, A_rows, AT_rows, B, BT):
+        """CSR variant of ``setup``: each argument is (rowptr, colidx[, values]) of
+        CUDA tensors (AT_rows and BT None together for symmetric inputs)."""
+        L = self.layout
+        self._csr_keep = (A_rows, AT_rows, B, BT)  # the library copies; keep until the call returns
+        st = [None if x is None else _lib.csr_struct_device(*x) for x in (A_rows, AT_rows, B, BT)]
+        ref = [None if c is None else ctypes.byref(c) for c in st]
+        _lib.check(self.lib.goat_shard_setup_csr(self.h.ptr, L.n, L.m, *ref))
+
     def gradient(self, Q_full, out):
         _lib.check(self.lib.goat_shard_gradient(self.h.ptr, Q_full.data_ptr(), out.data_ptr()))
 
@@ -215,7 +224,8 @@ def sharded_fw_core(backend, comm: Comm, A_rows, AT_rows, B, *, max_iters=30, ma
     L = backend.layout
     world = comm.world
     sense_code = _lib.GOAT_MAXIMIZE if sense == "maximize" else _lib.GOAT_MINIMIZE
-    backend.setup(A_rows, AT_rows, B)
+    if A_rows is not None:  # None: the caller already ran backend.setup_csr
+        backend.setup(A_rows, AT_rows, B)
     P, Q, G, GQ = backend.block(), backend.block(), backend.block(), backend.block()
     full = backend.full()
     send = backend.vec(L.n + 1)
@@ -291,15 +301,37 @@ def sharded_fw_core(backend, comm: Comm, A_rows, AT_rows, B, *, max_iters=30, ma
     return res
 
 
-def sharded_match(A: np.ndarray, B: np.ndarray, *, precision="fp32", group=None, gemm="auto",
-                  **kw) -> ShardedResult:
-    """Row-sharded GOAT on this rank's GPU for dense host A, B (every rank passes the
-    full matrices; each uploads only its own rows of A and A^T, and B)."""
+def _csr_rows_to_device(M, dev, dtype):
+    rowptr = torch.from_numpy(np.ascontiguousarray(M.indptr, dtype=np.int64)).to(dev)
+    col = torch.from_numpy(np.ascontiguousarray(M.indices, dtype=np.int32)).to(dev)
+    if np.all(M.data == 1.0):
+        return (rowptr, col)
+    return (rowptr, col, torch.from_numpy(np.ascontiguousarray(M.data)).to(dev, dtype))
+
+
+def sharded_match(A, B, *, precision="fp32", group=None, gemm="auto", **kw) -> ShardedResult:
+    """Row-sharded GOAT on this rank's GPU (every rank passes the full matrices;
+    each uploads only its own rows of A and A^T, and B).  Dense host arrays run the
+    GEMM gradient; scipy.sparse / CSR graphs run the SpMM gradient on CSR rows."""
+    from . import engine
     comm = Comm(group)
-    n = A.shape[0]
+    n = A.shape[0] if not isinstance(A, engine.CsrGraphType()) else A.n
     layout = ShardLayout(n, comm.world, comm.rank)
     be = GpuShardBackend(layout, precision, gemm=gemm)
     r0, m = layout.r0, layout.m
+    if engine.is_sparse(A) or engine.is_sparse(B):
+        A = engine.as_csr(A, "A")
+        B = engine.as_csr(B, "B")
+        sym = (A != A.T).nnz == 0 and (B != B.T).nnz == 0
+        dev, dt = be.dev, be.dtype
+        a_rows = _csr_rows_to_device(A[r0:r0 + m], dev, dt)
+        At = A.T.tocsr(); At.sort_indices()
+        at_rows = None if sym else _csr_rows_to_device(At[r0:r0 + m], dev, dt)
+        b_full = _csr_rows_to_device(B, dev, dt)
+        Bt = B.T.tocsr(); Bt.sort_indices()
+        bt_full = None if sym else _csr_rows_to_device(Bt, dev, dt)
+        be.setup_csr(a_rows, at_rows, b_full, bt_full)
+        return sharded_fw_core(be, comm, None, None, None, **kw)
     sym = bool(np.array_equal(A, A.T) and np.array_equal(B, B.T))
     A_rows = be.upload(A[r0:r0 + m], layout.m_pad)
     AT_rows = None if sym else be.upload(np.ascontiguousarray(A.T[r0:r0 + m]), layout.m_pad)

@@ -23,3 +23,24 @@ def test_lot_cluster_split_matches_oracle(n, precision):
     tol = 1e-3 if precision == "fp32" else 1e-5
     assert np.abs(res.matrix - Q).max() < tol
     assert res.deviation == pytest.approx(dev, rel=1e-2 if precision == "fp32" else 1e-6)
+
+
+@pytest.mark.parametrize("n", [10000, 20000])
+def test_fixed_shift_redo_path(n, monkeypatch):
+    """Wide fp32 rows use the previous row LSE as the exponent shift; a sweep with a
+    row outside the window is recomputed with the max shift.  Forcing every sweep
+    through the redo (GOAT_SK_RES=3) must give exactly the max-shift run
+    (GOAT_SK_RES=2), and the default run must agree with both to fp32 accuracy."""
+    rng = np.random.default_rng(n)
+    d1 = rng.integers(50, 150, n).astype(float)
+    d2 = rng.integers(50, 150, n).astype(float)
+    M = np.outer(d1, d2) / n + rng.random((n, n))
+    params = gb.SinkhornParams(max_sweeps=12)
+    out = {}
+    for mode in ("2", "3", "1"):
+        monkeypatch.setenv("GOAT_SK_RES", mode)
+        out[mode] = gb.lot(M, "maximize", params, precision="fp32")
+    assert np.array_equal(out["3"].matrix, out["2"].matrix)
+    assert out["3"].sweeps == out["2"].sweeps and out["3"].deviation == out["2"].deviation
+    assert np.abs(out["1"].matrix - out["2"].matrix).max() < 1e-5
+    assert out["1"].sweeps == out["2"].sweeps

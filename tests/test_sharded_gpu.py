@@ -94,3 +94,30 @@ def test_sharded_fp32_matches_unsharded(n, directed, iters):
     # two fp32 Sinkhorn arithmetics (single-pass max shift vs the unsharded
     # previous-LSE shift): the unconverged final LAP may move a percent of rows
     assert agree >= 0.98, agree
+
+
+@pytest.mark.parametrize("n,directed,seed", [(100, False, 1), (150, True, 2)])
+def test_sharded_csr_fp64_matches_oracle(n, directed, seed):
+    """Row-sharded iteration on CSR rows (SpMM gradient on the block) == oracle."""
+    import scipy.sparse as sp
+    A, B = _er_pair(n, 0.3, 0.8, directed, seed)
+    r = sharded_match(sp.csr_matrix(A), sp.csr_matrix(B), precision="fp64", max_iters=30)
+    tr = {}
+    a, hist, iters, conv = O.fw_core(A, B, None, np.full((n, n), 1.0 / n), trace=tr)
+    assert r.iterations == iters and r.converged == conv
+    assert r.lot_sweeps == tr["sweeps"]
+    np.testing.assert_allclose(r.hist_alpha[1:], [h[2] for h in hist[1:]], rtol=1e-7, atol=1e-12)
+    np.testing.assert_allclose(r.hist_obj, [h[1] for h in hist], rtol=1e-9)
+    assert list(r.assignment) == list(a)
+
+
+def test_sharded_csr_c5_n4000_matches_golden():
+    """Config 5 scaled to n = 4000 (CSR), row-sharded fp64: the oracle's recorded run."""
+    from paper_2111_05366_b200 import graphs
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c5_n4000.npz"))
+    A, Bs, truth = graphs.config_pair(5, 0, n=4000)
+    r = sharded_match(A, Bs, precision="fp64", max_iters=4)
+    assert r.iterations == int(g["iterations"]) and r.converged == bool(g["converged"])
+    np.testing.assert_array_equal(r.assignment, g["assignment"])
+    np.testing.assert_allclose(r.hist_alpha[1:], g["alpha"], atol=1e-6)
+    assert r.lot_sweeps == g["sweeps"].tolist()
