@@ -1162,33 +1162,37 @@ __device__ __forceinline__ void mbar_wait_cta(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-template <int NW, int CL> struct PipeSm {
+template <int NW, int CL, int R> struct PipeSm {
     uint64_t full[8], empty[8], wbar[4], xbar[4];
-    float wp[4][NW][2];  // per-warp (max, sum) of a band slot
-    float xp[4][CL][2];  // per-rank CTA (max, sum) of a band slot
+    float xp[4][CL][R][2];  // per-rank CTA (max, sum) of every row of a band slot
 };
 
 struct PipeRing {
     char *base;
-    int S, stage_bytes, nrows;
+    int S, stage_bytes, row_bytes, nrows, nbands;
     uint32_t copy_bytes;
     unsigned issued;  // bands issued (thread 0)
     unsigned used;    // bands consumed (all threads)
 };
 
-// Thread 0: issue every band below `upto` whose stage has been released.
-template <int NW, int CL>
-__device__ __forceinline__ void pipe_produce(const SkArgs &a, const Slice &sl, PipeRing &rg, PipeSm<NW, CL> &ps,
+// Thread 0: issue every band below `upto` whose stage has been released.  A band
+// is R rows of this group (local rows b*R .. b*R+R-1), one bulk copy per row.
+template <int NW, int CL, int R>
+__device__ __forceinline__ void pipe_produce(const SkArgs &a, const Slice &sl, PipeRing &rg, PipeSm<NW, CL, R> &ps,
                                              unsigned upto) {
     while (rg.issued < upto) {
-        if (a.single_pass && rg.issued >= (unsigned)rg.nrows) return;  // one sweep per launch
+        if (a.single_pass && rg.issued >= (unsigned)rg.nbands) return;  // one sweep per launch
         const unsigned u = rg.issued;
         const int s = (int)(u % (unsigned)rg.S);
         if (u >= (unsigned)rg.S) mbar_wait_cta(&ps.empty[s], ((u / (unsigned)rg.S) - 1) & 1);
-        const int row = sl.grp + (int)(u % (unsigned)rg.nrows) * sl.ngrp;
-        const float *src = static_cast<const float *>(a.G) + (int64_t)row * a.ld + sl.c0;
-        xbar_arm(&ps.full[s], rg.copy_bytes);
-        bulk_g2s(rg.base + (size_t)s * rg.stage_bytes, src, rg.copy_bytes, &ps.full[s]);
+        const int lr0 = (int)(u % (unsigned)rg.nbands) * R;
+        const int nv = min(R, rg.nrows - lr0);
+        xbar_arm(&ps.full[s], rg.copy_bytes * (uint32_t)nv);
+        for (int r = 0; r < nv; ++r) {
+            const int row = sl.grp + (lr0 + r) * sl.ngrp;
+            const float *src = static_cast<const float *>(a.G) + (int64_t)row * a.ld + sl.c0;
+            bulk_g2s(rg.base + (size_t)s * rg.stage_bytes + (size_t)r * rg.row_bytes, src, rg.copy_bytes, &ps.full[s]);
+        }
         ++rg.issued;
     }
 }
@@ -1204,15 +1208,15 @@ constexpr int kPipeShiftRows = 2048;
 constexpr float kShiftLo = 9.094947e-13f;   // 2^-40
 constexpr float kShiftHi = 1.2676506e30f;   // 2^100
 
-// Finish a band: f_k of the row (writer), the pre-check deviation, and the column
-// contributions acc += y * 2^(m_warp - lse) of this warp's exponentials.
-#define PIPE_FINISH(ITF, LSE, MWARP, YV)                                                        \
+// Finish one row of a band: f_k of the row (writer), the pre-check deviation, and
+// the column contributions acc += y * 2^(m_warp - lse) of this warp's exponentials.
+#define PIPE_FINISH(LR, LSE, MWARP, YV)                                                         \
     do {                                                                                        \
         const double lse_ = (LSE);                                                              \
         if (writer) {                                                                           \
             const double fnew = -lse_ * (1.0 / SkMath<T>::kScale);                              \
             if (pre) devmax = fmax(devmax, SkMath<T>::dev(-fnew));                              \
-            else __stcg(fout + sl.grp + (ITF) * sl.ngrp, fnew);                                 \
+            else __stcg(fout + sl.grp + (LR) * sl.ngrp, fnew);                                  \
         }                                                                                       \
         if (!rowonly && (MWARP) != neg_inf<T>()) {                                              \
             const T sc = SkMath<T>::ex((T)((double)(MWARP) + (pre ? 0.0 : -lse_)));             \
@@ -1221,9 +1225,9 @@ constexpr float kShiftHi = 1.2676506e30f;   // 2^100
         }                                                                                       \
     } while (0)
 
-template <int CH, int CL, int NT, bool MAXP>
+template <int CH, int CL, int NT, int R, bool MAXP>
 __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
-                                               const Slice &sl, PipeSm<NT / 32, CL> &ps, PipeRing &rg,
+                                               const Slice &sl, PipeSm<NT / 32, CL, R> &ps, PipeRing &rg,
                                                unsigned *redo) {
     using T = float;
     using V = float4;
@@ -1258,11 +1262,13 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
         }
         s_gl[tid + NT * c] = make_float4(gv[0], gv[1], gv[2], gv[3]);  // read back by this thread only
     }
-    // lagged state (clusters): the previous band's exponentials and warp max
+    // clusters: a band's exponentials wait in its stage for the lagged finish
     constexpr bool LAGGED = CL > 1;
-    T mp = neg_inf<T>();
+    T mp[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) mp[r] = neg_inf<T>();
     double devmax = 0.0;  // pre-check only (writer thread)
-    __shared__ T s_wp[2][NW][2];
+    __shared__ T s_wp[2][NW][R][2];
     __shared__ float s_shift[MAXP ? 1 : kPipeShiftRows];
     bool bad = false;
     if constexpr (!MAXP) {
@@ -1270,108 +1276,139 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
         __syncthreads();
     }
 
-    const int nrows = rg.nrows;
+    const int nrows = rg.nrows, nb = rg.nbands;
     const unsigned b0 = rg.used;
-    for (int it = 0; it < nrows + (LAGGED ? 1 : 0); ++it) {
+    for (int it = 0; it < nb + (LAGGED ? 1 : 0); ++it) {
         const unsigned b = b0 + (unsigned)it;
-        // keep S - 1 bands in flight beyond the one being loaded (never blocks in
-        // steady state: every warp passed the block barrier of band b - 1)
-        // (clusters: a stage is released only after its lagged finish, one band later)
-        if (tid == 0) pipe_produce<NW, CL>(a, sl, rg, ps, b + (unsigned)S - (LAGGED ? 2u : 1u));
-        T y[CH][VW];
-        T m = neg_inf<T>();
-        if (it < nrows) {
+        // keep the ring full (never blocks in steady state: every warp passed the
+        // block barrier of band b - 1); clusters release a stage one band later
+        if (tid == 0) pipe_produce<NW, CL, R>(a, sl, rg, ps, b + (unsigned)S - (LAGGED ? 2u : 1u));
+        T y[R][CH][VW];
+        T m[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) m[r] = neg_inf<T>();
+        if (it < nb) {
             const int s = (int)(b % (unsigned)S);
             mbar_wait_cta(&ps.full[s], (b / (unsigned)S) & 1);
-            const V *st = reinterpret_cast<const V *>(rg.base + (size_t)s * rg.stage_bytes);
 #pragma unroll
-            for (int c = 0; c < CH; ++c) {
-                const int col = c0 + (tid + NT * c) * VW;
-                V xv;
-                if (col < c1) xv = st[tid + NT * c];
-                else xv = make_float4(0.f, 0.f, 0.f, 0.f);
-                y[c][0] = xv.x; y[c][1] = xv.y; y[c][2] = xv.z; y[c][3] = xv.w;
+            for (int r = 0; r < R; ++r) {
+                const bool rv = it * R + r < nrows;
+                const V *st = reinterpret_cast<const V *>(rg.base + (size_t)s * rg.stage_bytes + (size_t)r * rg.row_bytes);
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const int col = c0 + (tid + NT * c) * VW;
+                    V xv;
+                    if (rv && col < c1) xv = st[tid + NT * c];
+                    else xv = make_float4(0.f, 0.f, 0.f, 0.f);
+                    y[r][c][0] = xv.x; y[r][c][1] = xv.y; y[r][c][2] = xv.z; y[r][c][3] = xv.w;
+                }
             }
             if constexpr (!LAGGED) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ps.empty[s]);
             }
-            if constexpr (MAXP) {
 #pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    const V g4 = s_gl[tid + NT * c];
-                    const T gl[VW] = {g4.x, g4.y, g4.z, g4.w};
+            for (int c = 0; c < CH; ++c) {
+                const V g4 = s_gl[tid + NT * c];
+                const T gl[VW] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+                for (int r = 0; r < R; ++r)
 #pragma unroll
                     for (int e = 0; e < VW; ++e) {
-                        const T arg = coef * (gmax - y[c][e]) + gl[e];  // E_ij + g_j (sinkhorn.py:125)
-                        y[c][e] = arg;
-                        m = vmax(m, arg);
+                        const T arg = coef * (gmax - y[r][c][e]) + gl[e];  // E_ij + g_j (sinkhorn.py:125)
+                        y[r][c][e] = arg;
+                        if constexpr (MAXP) m[r] = vmax(m[r], arg);
+                    }
+            }
+            if constexpr (MAXP) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) m[r] = vmax(m[r], __shfl_xor_sync(0xffffffffu, m[r], off));
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r)  // the row's shift, identical in every warp and cluster rank
+                    m[r] = (it * R + r < nrows) ? s_shift[it * R + r] : neg_inf<T>();
+            }
+            T sum[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool rv = it * R + r < nrows;
+                const T mx = (m[r] == neg_inf<T>()) ? T(0) : m[r];
+                T sp[VW];
+#pragma unroll
+                for (int e = 0; e < VW; ++e) sp[e] = T(0);
+#pragma unroll
+                for (int c = 0; c < CH; ++c)
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) {
+                        const T v = SkMath<T>::ex(y[r][c][e] - mx);
+                        y[r][c][e] = v;
+                        sp[e] += v;
+                    }
+                sum[r] = rv ? (sp[0] + sp[1]) + (sp[2] + sp[3]) : T(0);
+                if (!rv) m[r] = neg_inf<T>();
+            }
+            if constexpr (LAGGED) {
+                // the exponentials wait in the stage for the lagged finish
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    V *stw = reinterpret_cast<V *>(rg.base + (size_t)s * rg.stage_bytes + (size_t)r * rg.row_bytes);
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        const int col = c0 + (tid + NT * c) * VW;
+                        if (col < c1 && !rowonly)
+                            stw[tid + NT * c] = make_float4(y[r][c][0], y[r][c][1], y[r][c][2], y[r][c][3]);
                     }
                 }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) m = vmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-            } else {
-                m = s_shift[it];  // the row's shift, identical in every warp and cluster rank
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    const V g4 = s_gl[tid + NT * c];
-                    const T gl[VW] = {g4.x, g4.y, g4.z, g4.w};
-#pragma unroll
-                    for (int e = 0; e < VW; ++e) y[c][e] = coef * (gmax - y[c][e]) + gl[e];
-                }
-            }
-            const T mx = (m == neg_inf<T>()) ? T(0) : m;
-            T sp[VW];
-#pragma unroll
-            for (int e = 0; e < VW; ++e) sp[e] = T(0);
-#pragma unroll
-            for (int c = 0; c < CH; ++c)
-#pragma unroll
-                for (int e = 0; e < VW; ++e) {
-                    const T v = SkMath<T>::ex(y[c][e] - mx);
-                    y[c][e] = v;
-                    sp[e] += v;
-                }
-            T sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
-            if constexpr (LAGGED) {
-                // the exponentials wait in the stage for the lagged finish (registers
-                // stay free for one band: no spills at 128 registers/thread)
-                V *stw = reinterpret_cast<V *>(rg.base + (size_t)s * rg.stage_bytes);
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    const int col = c0 + (tid + NT * c) * VW;
-                    if (col < c1 && !rowonly) stw[tid + NT * c] = make_float4(y[c][0], y[c][1], y[c][2], y[c][3]);
-                }
             }
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-            if (lane == 0) { s_wp[b & 1][warp][0] = m; s_wp[b & 1][warp][1] = sum; }
+            for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                for (int r = 0; r < R; ++r) sum[r] += __shfl_xor_sync(0xffffffffu, sum[r], off);
+            if (lane == 0) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) { s_wp[b & 1][warp][r][0] = m[r]; s_wp[b & 1][warp][r][1] = sum[r]; }
+            }
             __syncthreads();
-            // every warp combines the NW warp pairs (fixed tree: identical in all warps)
-            T M, Sm;
-            if constexpr (MAXP) {
-                const T mv = lane < NW ? s_wp[b & 1][lane][0] : neg_inf<T>();
-                M = mv;
+            // every warp combines the NW warp pairs of each row (fixed tree: identical in all warps)
+            T M[R], Sm[R];
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) M = vmax(M, __shfl_xor_sync(0xffffffffu, M, off));
-                Sm = (mv != neg_inf<T>()) ? s_wp[b & 1][lane][1] * SkMath<T>::ex(mv - M) : T(0);
-            } else {
-                M = m;
-                Sm = lane < NW ? s_wp[b & 1][lane][1] : T(0);
+            for (int r = 0; r < R; ++r) {
+                if constexpr (MAXP) {
+                    const T mv = lane < NW ? s_wp[b & 1][lane][r][0] : neg_inf<T>();
+                    M[r] = mv;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) M[r] = vmax(M[r], __shfl_xor_sync(0xffffffffu, M[r], off));
+                    Sm[r] = (mv != neg_inf<T>()) ? s_wp[b & 1][lane][r][1] * SkMath<T>::ex(mv - M[r]) : T(0);
+                } else {
+                    M[r] = m[r];
+                    Sm[r] = lane < NW ? s_wp[b & 1][lane][r][1] : T(0);
+                }
             }
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) Sm += __shfl_xor_sync(0xffffffffu, Sm, off);
+            for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                for (int r = 0; r < R; ++r) Sm[r] += __shfl_xor_sync(0xffffffffu, Sm[r], off);
             if constexpr (!LAGGED) {
-                if constexpr (!MAXP) bad |= !(Sm >= kShiftLo && Sm <= kShiftHi) || a.resident == 3;
-                PIPE_FINISH(it, (double)M + SkMath<T>::lgt(Sm), m, y);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (it * R + r >= nrows) continue;
+                    if constexpr (!MAXP) bad |= !(Sm[r] >= kShiftLo && Sm[r] <= kShiftHi) || a.resident == 3;
+                    PIPE_FINISH(it * R + r, (double)M[r] + SkMath<T>::lgt(Sm[r]), m[r], y[r]);
+                }
             } else {
-                // this CTA's pair -> every rank of the cluster; finished next band
+                // this CTA's pairs -> every rank of the cluster; finished next band
                 const int xs = (int)(b & 3);
                 if (warp == 0) {
-                    if (lane == 0) xbar_arm(&ps.xbar[xs], (uint32_t)(CL * 2 * sizeof(T)));
+                    if (lane == 0) xbar_arm(&ps.xbar[xs], (uint32_t)(CL * R * 2 * sizeof(T)));
                     __syncwarp();
-                    if (lane < CL)
-                        st_async_pair(dsmem_map(&ps.xp[xs][sl.rank][0], lane), M, Sm, dsmem_map(&ps.xbar[xs], lane));
+                    if (lane < CL) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            st_async_pair(dsmem_map(&ps.xp[xs][sl.rank][r][0], lane), M[r], Sm[r],
+                                          dsmem_map(&ps.xbar[xs], lane));
+                    }
                 }
             }
         }
@@ -1379,48 +1416,57 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
             if (it >= 1) {
                 const unsigned bf = b - 1;
                 const int xs = (int)(bf & 3);
-                T mq[CL], sq[CL];
+                T mq[R][CL], sq[R][CL];
                 if (lane == 0) {
                     xbar_wait(&ps.xbar[xs], (bf >> 2) & 1);
 #pragma unroll
-                    for (int q = 0; q < CL; ++q) { mq[q] = ps.xp[xs][q][0]; sq[q] = ps.xp[xs][q][1]; }
-                }
+                    for (int r = 0; r < R; ++r)
 #pragma unroll
-                for (int q = 0; q < CL; ++q) {
-                    mq[q] = __shfl_sync(0xffffffffu, mq[q], 0);
-                    sq[q] = __shfl_sync(0xffffffffu, sq[q], 0);
-                }
-                T M = neg_inf<T>(), Sm = T(0);
-                if constexpr (MAXP) {
-#pragma unroll
-                    for (int q = 0; q < CL; ++q) M = vmax(M, mq[q]);
-#pragma unroll
-                    for (int q = 0; q < CL; ++q)
-                        if (mq[q] != neg_inf<T>()) Sm += sq[q] * SkMath<T>::ex(mq[q] - M);
-                } else {
-                    M = mq[0];  // the common shift
-#pragma unroll
-                    for (int q = 0; q < CL; ++q) Sm += sq[q];
-                    bad |= !(Sm >= kShiftLo && Sm <= kShiftHi) || a.resident == 3;
+                        for (int q = 0; q < CL; ++q) { mq[r][q] = ps.xp[xs][q][r][0]; sq[r][q] = ps.xp[xs][q][r][1]; }
                 }
                 const int sf = (int)(bf % (unsigned)S);
-                const V *stf = reinterpret_cast<const V *>(rg.base + (size_t)sf * rg.stage_bytes);
-                T yl[CH][VW];
 #pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    const int col = c0 + (tid + NT * c) * VW;
-                    const V yv = (col < c1 && !rowonly) ? stf[tid + NT * c] : make_float4(0.f, 0.f, 0.f, 0.f);
-                    yl[c][0] = yv.x; yl[c][1] = yv.y; yl[c][2] = yv.z; yl[c][3] = yv.w;
+                for (int r = 0; r < R; ++r) {
+#pragma unroll
+                    for (int q = 0; q < CL; ++q) {
+                        mq[r][q] = __shfl_sync(0xffffffffu, mq[r][q], 0);
+                        sq[r][q] = __shfl_sync(0xffffffffu, sq[r][q], 0);
+                    }
+                    const int lr = (it - 1) * R + r;
+                    if (lr >= nrows) continue;
+                    T M = neg_inf<T>(), Sm = T(0);
+                    if constexpr (MAXP) {
+#pragma unroll
+                        for (int q = 0; q < CL; ++q) M = vmax(M, mq[r][q]);
+#pragma unroll
+                        for (int q = 0; q < CL; ++q)
+                            if (mq[r][q] != neg_inf<T>()) Sm += sq[r][q] * SkMath<T>::ex(mq[r][q] - M);
+                    } else {
+                        M = mq[r][0];  // the common shift
+#pragma unroll
+                        for (int q = 0; q < CL; ++q) Sm += sq[r][q];
+                        bad |= !(Sm >= kShiftLo && Sm <= kShiftHi) || a.resident == 3;
+                    }
+                    const V *stf = reinterpret_cast<const V *>(rg.base + (size_t)sf * rg.stage_bytes +
+                                                               (size_t)r * rg.row_bytes);
+                    T yl[CH][VW];
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        const int col = c0 + (tid + NT * c) * VW;
+                        const V yv = (col < c1 && !rowonly) ? stf[tid + NT * c] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        yl[c][0] = yv.x; yl[c][1] = yv.y; yl[c][2] = yv.z; yl[c][3] = yv.w;
+                    }
+                    PIPE_FINISH(lr, (double)M + SkMath<T>::lgt(Sm), mp[r], yl);
                 }
                 fence_proxy_async_smem();  // this thread's stage accesses precede the bulk refill
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ps.empty[sf]);
-                PIPE_FINISH(it - 1, (double)M + SkMath<T>::lgt(Sm), mp, yl);
             }
-            mp = m;
+#pragma unroll
+            for (int r = 0; r < R; ++r) mp[r] = m[r];
         }
     }
-    rg.used = b0 + (unsigned)nrows;
+    rg.used = b0 + (unsigned)nb;
     if (!rowonly) {
         T *cp = static_cast<T *>(a.colpart) + (int64_t)sl.grp * a.ldp;
 #pragma unroll
@@ -1457,7 +1503,7 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
 // for a redo (tests of the redo path)
 __device__ __forceinline__ bool env_shift_ok(const SkArgs &a) { return a.resident != 2; }
 
-template <int CH, int CL, int NT>
+template <int CH, int CL, int NT, int R>
 __global__ void __launch_bounds__(NT, 1) sk_pipe_kernel(SkArgs a, unsigned *bar) {
     using T = float;
     constexpr int NW = NT / 32;
@@ -1481,13 +1527,15 @@ __global__ void __launch_bounds__(NT, 1) sk_pipe_kernel(SkArgs a, unsigned *bar)
         sl.c0 = min(a.n, (int)rank * a.slice_w);
         sl.c1 = min(a.n, sl.c0 + a.slice_w);
     }
-    __shared__ PipeSm<NW, CL> ps;
+    __shared__ PipeSm<NW, CL, R> ps;
     extern __shared__ __align__(128) char sk_ring[];
     PipeRing rg;
     rg.base = sk_ring;
     rg.S = a.stages;
     rg.stage_bytes = a.stage_bytes;
+    rg.row_bytes = a.stage_bytes / R;
     rg.nrows = (rows_of(a) - sl.grp + sl.ngrp - 1) / sl.ngrp;
+    rg.nbands = (max(rg.nrows, 0) + R - 1) / R;
     rg.copy_bytes = (uint32_t)(((sl.c1 - sl.c0 + 3) / 4) * sizeof(float4));
     rg.issued = 0;
     rg.used = 0;
@@ -1498,7 +1546,7 @@ __global__ void __launch_bounds__(NT, 1) sk_pipe_kernel(SkArgs a, unsigned *bar)
     }
     if constexpr (CL > 1) cluster_sync();  // every peer's barriers exist before the first st.async
     else __syncthreads();
-    if (rg.nrows <= 0) rg.nrows = 0;
+    if (rg.nrows <= 0) { rg.nrows = 0; rg.nbands = 0; }
     unsigned epoch = 0;
     auto drain = [&]() {  // no bulk copy may be in flight when the CTA exits
         if (threadIdx.x == 0)
@@ -1513,8 +1561,8 @@ __global__ void __launch_bounds__(NT, 1) sk_pipe_kernel(SkArgs a, unsigned *bar)
         bool maxp = !shift_ok || k <= 1;
         for (;;) {
             if (rg.nrows > 0) {
-                if (maxp) pass_body_pipe<CH, CL, NT, true>(a, k, K, coef, gmax, sl, ps, rg, redo + (k & 1));
-                else pass_body_pipe<CH, CL, NT, false>(a, k, K, coef, gmax, sl, ps, rg, redo + (k & 1));
+                if (maxp) pass_body_pipe<CH, CL, NT, R, true>(a, k, K, coef, gmax, sl, ps, rg, redo + (k & 1));
+                else pass_body_pipe<CH, CL, NT, R, false>(a, k, K, coef, gmax, sl, ps, rg, redo + (k & 1));
             } else if (threadIdx.x == 0) {
                 __stcg(a.devpart + blockIdx.x, 0.0);
             }
@@ -1901,28 +1949,33 @@ cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunch
 
 }  // namespace
 
-template <int CH, int CL> void *pipe_fn() { return (void *)sk_pipe_kernel<CH, CL, kWideThreads>; }
+template <int CH, int CL, int R> void *pipe_fn() { return (void *)sk_pipe_kernel<CH, CL, kWideThreads, R>; }
 
-void *pipe_for(int ch, int cl, int nt) {
-#define GOAT_PCL(C)                                       \
-    if (nt == kWideThreads && cl == C) {                  \
-        switch (ch) {                                     \
-            case 3: return pipe_fn<3, C>();               \
-            case 4: return pipe_fn<4, C>();               \
-            case 5: return pipe_fn<5, C>();               \
-            case 6: return pipe_fn<6, C>();               \
-            case 7: return pipe_fn<7, C>();               \
-        }                                                 \
+void *pipe_for(int ch, int cl, int nt, int rows) {
+#define GOAT_PCL(C)                                                 \
+    if (nt == kWideThreads && cl == C && rows == 1) {               \
+        switch (ch) {                                               \
+            case 3: return pipe_fn<3, C, 1>();                      \
+            case 4: return pipe_fn<4, C, 1>();                      \
+            case 5: return pipe_fn<5, C, 1>();                      \
+            case 6: return pipe_fn<6, C, 1>();                      \
+            case 7: return pipe_fn<7, C, 1>();                      \
+        }                                                           \
+    }                                                               \
+    if (nt == kWideThreads && cl == C && rows == 2) {               \
+        switch (ch) {                                               \
+            case 3: return pipe_fn<3, C, 2>();                      \
+            case 4: return pipe_fn<4, C, 2>();                      \
+            case 5: return pipe_fn<5, C, 2>();                      \
+        }                                                           \
     }
     GOAT_PCL(1)
     GOAT_PCL(2)
-    GOAT_PCL(3)
     GOAT_PCL(4)
-    GOAT_PCL(6)
     GOAT_PCL(8)
 #undef GOAT_PCL
     throw Error(GOAT_ENOTSUP, "sinkhorn: no pipelined kernel for chunks=" + std::to_string(ch) + " cluster=" +
-                                  std::to_string(cl));
+                                  std::to_string(cl) + " rows=" + std::to_string(rows));
 }
 
 // Wide fp32 rows: the decoupled bulk-copy pipeline (sk_pipe_kernel), one
@@ -1953,22 +2006,23 @@ bool pipe_plan(int n, int mrows, SkPlan &p) {
         const int maxch = std::min(7, env_int("GOAT_SK_PIPE_CH", 7));
         const int force = env_int("GOAT_SK_PIPE_CL", 0);
         bool found = false;
-        for (int cl : {2, 3, 4, 6, 8}) {
-            if (force ? cl != force : (cl != lcl && env_int("GOAT_SK_PIPE", 1) != 2) || cl == 3 || cl == 6) continue;
+        const int R = std::max(1, std::min(2, env_int("GOAT_SK_PIPE_R", 1)));
+        for (int cl : {2, 4, 8}) {
+            if (force ? cl != force : (cl != lcl && env_int("GOAT_SK_PIPE", 1) != 2 && R == 1)) continue;
             const int sw = (int)round_up(ceil_div(n, cl), 8 * VW);
             const int ch = std::max(3, ceil_div(ceil_div(sw, VW), p.nt));
-            const size_t stage = round_up((size_t)sw * sizeof(float), 128), glb = (size_t)p.nt * ch * 16;
-            if (ch > maxch || (220 * 1024 - glb) / stage < 4) continue;
-            p.cl = cl; p.slice_w = sw; p.ch = ch;
+            const size_t stage = R * round_up((size_t)sw * sizeof(float), 128), glb = (size_t)p.nt * ch * 16;
+            if (ch > (R == 1 ? maxch : 5) || (220 * 1024 - glb) / stage < 4) continue;
+            p.cl = cl; p.slice_w = sw; p.ch = ch; p.rows = R;
             found = true;
             break;
         }
         if (!found) return false;
     }
-    p.rows = 1;
+    if (p.cl == 1) p.rows = 1;
     p.pipe = true;
-    // ring stages + one more slice for g (scaled), within ~216 KB of dynamic smem
-    p.stage_bytes = (int)round_up((size_t)p.slice_w * sizeof(float), 128);
+    // ring stages (R row slices each) + one more slice for g (scaled)
+    p.stage_bytes = p.rows * (int)round_up((size_t)p.slice_w * sizeof(float), 128);
     const size_t gl_bytes = (size_t)p.nt * p.ch * 16;  // every thread's chunks, masked ones included
     p.stages = std::min(8, (int)((220 * 1024 - gl_bytes) / p.stage_bytes));
     if (const int st = env_int("GOAT_SK_STAGES", 0)) p.stages = std::min(p.stages, std::max(3, st));
@@ -1984,7 +2038,7 @@ template <class T> SkPlan sk_plan(int n, int num_sms, int mrows) {
     SkPlan p;
     if (sizeof(T) == 4 && ceil_div(ceil_div(n, VW), kThreads) > kMaxCh && env_int("GOAT_SK_PIPE", 1) &&
         pipe_plan(n, mrows, p)) {
-        void *const kfn = pipe_for(p.ch, p.cl, p.nt);
+        void *const kfn = pipe_for(p.ch, p.cl, p.nt, p.rows);
         GOAT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
         if (p.cl > 1) GOAT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         p.persistent = true;
@@ -2120,7 +2174,7 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
     void *params[] = {&args, &bar};
     cudaLaunchAttribute attrs[2];
     cudaLaunchConfig_t cfg = persistent_config(p, s, attrs);
-    void *fn = p.pipe ? pipe_for(p.ch, p.cl, p.nt) : persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
+    void *fn = p.pipe ? pipe_for(p.ch, p.cl, p.nt, p.rows) : persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
     GOAT_CUDA(cudaLaunchKernelExC(&cfg, fn, params));
     note_launch();
 }
