@@ -296,11 +296,13 @@ def run_ours(args):
         "e2e": {"value": e2e_iters_all / (e2e_max / 1000.0), "unit": "iter/s",
                 "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * 8 + 8 * 2 * 31,
                 "time_to_converge_ms": e2e_max / args.steps},
-        "roofline": {"kernel": "sk_pass_kernel (fused log-domain Sinkhorn sweep)", "bound": "hbm",
+        "roofline": {"kernel": "sk_tile_kernel (persistent log-domain Sinkhorn LOT, one read of G per sweep)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_kind": peak_kind, "traffic": None,
-                     "note": f"{bytes_per_sweep} algorithmic bytes/launch (n^2 fp32, one read of G); "
-                             f"{msw * 1000:.2f} us/launch; at n=1000 G is L2-resident"},
+                     "note": f"{bytes_per_sweep} algorithmic bytes per sweep (n^2 fp32, one read of G), "
+                             f"{msw * 1000:.2f} us per sweep; at n=1000 the G tiles stay in shared memory "
+                             f"for the whole LOT, so the sweep is latency-bound (one grid barrier, one "
+                             f"DSMEM row exchange, one L2 column merge), not HBM-bound"},
         "cpu_baseline": {k: v for k, v in cpu.items()},
         "kernels": kernels,
         "c5": c5,

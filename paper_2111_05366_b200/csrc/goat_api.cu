@@ -1428,7 +1428,7 @@ int goat_shard_setup(goat_handle *h, int64_t n, int64_t m, const void *dA_rows, 
         if (S.tc) shard_tc_prepare(*h);
         dispatch(*h, [&](auto *tag) {
             using T = std::remove_pointer_t<decltype(tag)>;
-            S.plan = sk_plan<T>((int)n, h->num_sms, (int)m);
+            S.plan = sk_plan<T>((int)n, h->num_sms, (int)m, true);
         });
         h->colpart.ensure(S.plan.colpart_bytes);
         S.bad.ensure((size_t)ld_for(n));
@@ -1483,7 +1483,7 @@ int goat_shard_setup_csr(goat_handle *h, int64_t n, int64_t m, const goat_csr *d
         GOAT_CUDA(cudaMemsetAsync(S.X.p, 0, S.X.bytes, s));
         dispatch(*h, [&](auto *tag) {
             using T = std::remove_pointer_t<decltype(tag)>;
-            S.plan = sk_plan<T>((int)n, h->num_sms, (int)m);
+            S.plan = sk_plan<T>((int)n, h->num_sms, (int)m, true);
         });
         h->colpart.ensure(S.plan.colpart_bytes);
         S.bad.ensure((size_t)ld_for(n));

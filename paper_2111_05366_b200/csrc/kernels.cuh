@@ -46,10 +46,13 @@ struct SkPlan {
     int stage_bytes = 0;
     size_t smem = 0;          // dynamic shared memory of the persistent kernel
     bool pipe = false;        // wide fp32 rows: decoupled bulk-copy pipeline (sk_pipe_kernel)
+    bool tile = false;        // small n: shared-memory-resident tiles, one barrier per sweep (sk_tile_kernel)
+    int tile_rows = 0;        // rows per row group of the tile kernel
 };
 
-// rows: rows of a row-sharded block (-1 = n).
-template <class T> SkPlan sk_plan(int n, int num_sms, int rows = -1);
+// rows: rows of a row-sharded block (-1 = n); sharded: the plan serves single-pass
+// launches of the row-sharded driver (no whole-LOT tile kernel).
+template <class T> SkPlan sk_plan(int n, int num_sms, int rows = -1, bool sharded = false);
 template <class T> void sk_launch_pass(const SkArgs &a, const SkPlan &p, cudaStream_t s);
 template <class T> void sk_launch_merge(const SkArgs &a, const SkPlan &p, cudaStream_t s);
 // All sweeps in one cooperative launch (bar: 2 unsigned of scratch).

@@ -1947,6 +1947,249 @@ cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunch
 }
 
 
+
+// ------------------------------------------------------------------ small-n tile kernel
+// n <= ~2500 (fp32): the LOT is latency bound (a sweep of the lock-step kernel
+// is ~3.5 us of pass plus two grid barriers and a distributed merge, at n = 64
+// as at n = 1000).  Here a thread-block cluster of CL CTAs owns a group of rows,
+// CTA rank q the column slice q, and the G tile stays in shared memory for the
+// whole LOT.  One warp covers a row's slice, so a row's (max, sum) pair needs
+// only a warp butterfly; the CL pairs of a row meet through DSMEM (st.async +
+// mbarrier) and every CTA combines them in rank order.  After the single grid
+// barrier of a sweep every CTA merges the column partials of ITS OWN slice
+// (fixed order over the row groups): the same-rank CTAs of every cluster compute
+// the same g slice redundantly, so there is no second barrier and no reload of g.
+constexpr int kTileThreads = 512;
+constexpr int kTileWarps = kTileThreads / 32;
+
+template <class T, int CL, int CPL, int RPW>
+__global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsigned *bar, int rows_g) {
+    constexpr int SW = 32 * CPL;  // slice width held per CTA (columns, padded)
+    constexpr int NW = kTileWarps;
+    extern __shared__ __align__(16) unsigned char tsm[];
+    T *tile = reinterpret_cast<T *>(tsm);                                 // [rows_g][SW]
+    T *wpart = tile + (size_t)rows_g * SW;                                // [NW][SW]
+    double *gsl = reinterpret_cast<double *>(wpart + (size_t)NW * SW);   // [SW] g (natural units)
+    T *gst = reinterpret_cast<T *>(gsl + SW);                              // [SW] g scaled (-inf: masked)
+    double *fpr = reinterpret_cast<double *>(gst + SW + (SW & 1));        // [rows_g] f_{k-1} of the group's rows
+    T *xp = reinterpret_cast<T *>(fpr + rows_g);                          // [2][CL][rows_g][2]
+    __shared__ uint64_t xbar[2];
+    __shared__ double s_red[NW];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t rank = 0, cid = blockIdx.x, ncl = gridDim.x;
+    if constexpr (CL > 1) {
+        asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+        asm("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
+    }
+    const int n = a.n, grp = (int)cid, ngrp = (int)ncl;
+    const int c0 = min(n, (int)rank * a.slice_w), c1 = min(n, c0 + a.slice_w);
+    const int r0 = grp * rows_g, nr = max(0, min(rows_g, n - r0));  // rows [r0, r0 + nr)
+    const int K = a.st->max_sweeps;
+    const double tol = a.st->tol, coef_d = a.st->coef, gmax_d = a.st->gmax;
+    const double ks = SkMath<T>::kScale;
+    const T coef = (T)(coef_d * ks), gmax = (T)gmax_d;
+    const int k0 = a.st->k;
+    const T *G = static_cast<const T *>(a.G);
+    // tile, g slice (from slot k0+1), barriers
+    for (int idx = tid; idx < rows_g * SW; idx += kTileThreads) {
+        const int r = idx / SW, c = idx % SW;
+        tile[idx] = (r < nr && c0 + c < c1) ? G[(int64_t)(r0 + r) * a.ld + c0 + c] : T(0);
+    }
+    for (int c = tid; c < SW; c += kTileThreads) {
+        const bool ok = c0 + c < c1;
+        // g_{k0-1}: zero before sweep 1 (the pre-check uses no g; slot 1 may hold a
+        // previous LOT's potentials)
+        const double gv = (ok && k0 >= 1) ? __ldcg(gslot(a, k0 + 1) + c0 + c) : 0.0;
+        gsl[c] = gv;
+        gst[c] = ok ? (T)(gv * ks) : neg_inf<T>();
+    }
+    if (tid == 0) {
+        xbar_init(&xbar[0]);
+        xbar_init(&xbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if constexpr (CL > 1) cluster_sync();
+    else __syncthreads();
+
+    const bool writer = rank == 0 && lane == 0;
+    unsigned epoch = 0;
+    int par = 0;
+    for (int k = k0;; ++k, par ^= 1) {
+        const bool pre = (k == 0), rowonly = (k == K + 1);
+        double *fout = fslot(a, k);
+        if (tid == 0) xbar_arm(&xbar[par], (uint32_t)(CL * nr * 2 * sizeof(T)));
+        // ---- rows: warp w owns rows w, w + NW, ...
+        T y[RPW][CPL], mw[RPW];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int r = warp + NW * i;
+            mw[i] = neg_inf<T>();
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const T arg = (r < nr) ? coef * (gmax - tile[r * SW + lane + 32 * q]) + gst[lane + 32 * q]
+                                       : neg_inf<T>();  // E_ij + g_j (sinkhorn.py:125)
+                y[i][q] = arg;
+                mw[i] = vmax(mw[i], arg);
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) mw[i] = vmax(mw[i], __shfl_xor_sync(0xffffffffu, mw[i], off));
+        T sw[RPW];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const T mx = (mw[i] == neg_inf<T>()) ? T(0) : mw[i];
+            T sp = T(0);
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                y[i][q] = SkMath<T>::ex(y[i][q] - mx);
+                sp += y[i][q];
+            }
+            sw[i] = sp;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) sw[i] += __shfl_xor_sync(0xffffffffu, sw[i], off);
+        // this CTA's pair of each row -> every rank (incl. itself)
+        if (lane < CL) {
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int r = warp + NW * i;
+                if (r < nr) {
+                    T *slot = xp + (((size_t)par * CL + rank) * rows_g + r) * 2;
+                    if constexpr (CL > 1)
+                        st_async_pair(dsmem_map(slot, (uint32_t)lane), mw[i], sw[i], dsmem_map(&xbar[par], (uint32_t)lane));
+                    else
+                        st_async_pair((uint32_t)__cvta_generic_to_shared(slot), mw[i], sw[i],
+                                      (uint32_t)__cvta_generic_to_shared(&xbar[par]));
+                }
+            }
+        }
+        xbar_wait(&xbar[par], (uint32_t)((k - k0) >> 1) & 1u);
+        double devmax = 0.0;
+        T sc[RPW];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int r = warp + NW * i;
+            sc[i] = T(0);
+            if (r >= nr) continue;
+            T M = neg_inf<T>();
+#pragma unroll
+            for (int q = 0; q < CL; ++q) M = vmax(M, xp[(((size_t)par * CL + q) * rows_g + r) * 2]);
+            T S = T(0);
+#pragma unroll
+            for (int q = 0; q < CL; ++q) {
+                const T mq = xp[(((size_t)par * CL + q) * rows_g + r) * 2];
+                if (mq != neg_inf<T>()) S += xp[(((size_t)par * CL + q) * rows_g + r) * 2 + 1] * SkMath<T>::ex(mq - M);
+            }
+            const double lse = (double)M + SkMath<T>::lgt(S);  // scaled units
+            const double fnew = -lse * (1.0 / ks);
+            if (writer) {
+                double dev = 0.0;
+                if (pre) dev = SkMath<T>::dev(-fnew);                  // |rowsum(K) - 1|
+                else if (k >= 2) dev = SkMath<T>::dev(fpr[r] - fnew);  // |u K v - 1|
+                if (!pre) { __stcg(fout + r0 + r, fnew); fpr[r] = fnew; }
+                devmax = fmax(devmax, dev);
+            }
+            if (!rowonly && mw[i] != neg_inf<T>())
+                sc[i] = SkMath<T>::ex((T)((double)mw[i] + (pre ? 0.0 : -lse)));
+        }
+        if (!rowonly) {
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                T cp = T(0);
+#pragma unroll
+                for (int i = 0; i < RPW; ++i) cp += y[i][q] * sc[i];
+                wpart[warp * SW + lane + 32 * q] = cp;
+            }
+        }
+        if (lane == 0) s_red[warp] = devmax;
+        __syncthreads();
+        if (!rowonly) {
+            T *cp = static_cast<T *>(a.colpart) + (int64_t)grp * a.ldp;
+            for (int c = tid; c < SW; c += kTileThreads) {
+                if (c0 + c >= c1) continue;
+                T v = T(0);
+#pragma unroll
+                for (int w = 0; w < NW; ++w) v += wpart[w * SW + c];
+                __stcg(cp + c0 + c, v);
+            }
+        }
+        if (tid == 0) {
+            double d = 0.0;
+            for (int w = 0; w < NW; ++w) d = fmax(d, s_red[w]);
+            // three rotating slots [3 + k % 3]: with one barrier per sweep a slot is
+            // cleared a full sweep before its next use (see below)
+            if (d > 0.0) atomicMax(a.dslot + 3 + (k % 3), (unsigned long long)__double_as_longlong(d));
+        }
+        grid_barrier(bar, gridDim.x, epoch);
+        const double drow = __longlong_as_double((long long)__ldcg(a.dslot + 3 + (k % 3)));
+        int stop = 0, sweeps = 0, conv = 0, slot = 0;
+        if (k >= 2) {
+            if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
+            else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
+        }
+        if (stop) {
+            if (blockIdx.x == 0 && tid == 0) {
+                a.st->dev = drow;
+                a.st->done = 1; a.st->sweeps = sweeps; a.st->converged = conv; a.st->slot = slot;
+                a.st->k = k + 1;
+            }
+            break;
+        }
+        // ---- merge of this CTA's columns (fixed order over the row groups, fp64)
+        const T *cpa = static_cast<const T *>(a.colpart);
+        const double tiny = sizeof(T) == 4 ? 1e-30 : 1e-290;
+        double dloc = 0.0;
+        for (int c = tid; c < SW; c += kTileThreads) {
+            const int j = c0 + c;
+            if (j >= c1) continue;
+            double Ssum = 0.0;
+            for (int g = 0; g < ngrp; ++g) Ssum += (double)__ldcg(cpa + (int64_t)g * a.ldp + j);
+            if (pre) {
+                if (!(Ssum > tiny)) Ssum = exp(-sk_exact_col<T>(G, a.ld, n, j, nullptr, true, coef_d, gmax_d));
+                dloc = fmax(dloc, fabs(Ssum - 1.0));
+            } else {
+                double gnew = gsl[c] - log(Ssum);
+                if (!(Ssum > tiny) || !isfinite(Ssum)) gnew = sk_exact_col<T>(G, a.ld, n, j, fout, false, coef_d, gmax_d);
+                gsl[c] = gnew;
+                gst[c] = (T)(gnew * ks);
+                if (grp == 0) __stcg(gslot(a, k) + j, gnew);
+            }
+        }
+        // slot of sweep k+2: last read after the barrier of sweep k-1, next written after barrier k+1
+        if (blockIdx.x == 0 && tid == 0) a.dslot[3 + ((k + 2) % 3)] = 0ull;
+        if (pre) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) dloc = fmax(dloc, __shfl_xor_sync(0xffffffffu, dloc, off));
+            if (lane == 0) s_red[warp] = dloc;
+            __syncthreads();
+            if (tid == 0) {
+                double d = 0.0;
+                for (int w = 0; w < NW; ++w) d = fmax(d, s_red[w]);
+                atomicMax(a.dslot + 2, (unsigned long long)__double_as_longlong(d));
+            }
+            grid_barrier(bar, gridDim.x, epoch);  // pre-check only: the column deviation is global
+            const double d0 = fmax(drow, __longlong_as_double((long long)__ldcg(a.dslot + 2)));
+            if (blockIdx.x == 0 && tid == 0) a.st->last_dev = d0;
+            if (d0 < tol) {
+                if (blockIdx.x == 0 && tid == 0) {
+                    a.st->dev = d0;
+                    a.st->done = 1; a.st->sweeps = 0; a.st->converged = 1; a.st->slot = 0;
+                    a.st->k = k + 1;
+                }
+                break;
+            }
+        }
+        __syncthreads();  // the new g slice before the next pass
+    }
+    if constexpr (CL > 1) cluster_sync();  // no CTA leaves while peers may still write into it
+}
+
 }  // namespace
 
 template <int CH, int CL, int R> void *pipe_fn() { return (void *)sk_pipe_kernel<CH, CL, kWideThreads, R>; }
@@ -2032,10 +2275,99 @@ bool pipe_plan(int n, int mrows, SkPlan &p) {
     return true;
 }
 
-template <class T> SkPlan sk_plan(int n, int num_sms, int mrows) {
+template <class T, int CL, int CPL, int RPW> void *tile_fn() { return (void *)sk_tile_kernel<T, CL, CPL, RPW>; }
+
+template <class T> void *tile_for(int cl, int cpl, int rpw) {
+#define GOAT_TL(C, P)                                          \
+    if (cl == C && cpl == P) {                                 \
+        switch (rpw) {                                         \
+            case 1: return tile_fn<T, C, P, 1>();              \
+            case 2: return tile_fn<T, C, P, 2>();              \
+            case 3: return tile_fn<T, C, P, 3>();              \
+            case 4: return tile_fn<T, C, P, 4>();              \
+        }                                                      \
+    }
+    GOAT_TL(2, 1) GOAT_TL(2, 2) GOAT_TL(2, 4) GOAT_TL(2, 8)
+    GOAT_TL(4, 1) GOAT_TL(4, 2) GOAT_TL(4, 4) GOAT_TL(4, 8) GOAT_TL(4, 16)
+#undef GOAT_TL
+    return nullptr;
+}
+
+template <class T> size_t tile_smem(int rows_g, int sw, int cl) {
+    return (size_t)rows_g * sw * sizeof(T) + (size_t)kTileWarps * sw * sizeof(T) + (size_t)sw * 8 +
+           (size_t)sw * sizeof(T) + (size_t)rows_g * 8 + (size_t)2 * cl * rows_g * 2 * sizeof(T);
+}
+
+template <class T> bool tile_plan_width(int n, int num_sms, SkPlan &p, int cl, int cpl) {
+    const int sw = 32 * cpl;
+    int ncl = 0;
+    {
+        // co-resident clusters with the largest shared-memory footprint this n can need
+        int rows_guess = (int)round_up(ceil_div(n, std::max(1, num_sms / cl)), 2);
+        void *fn = tile_for<T>(cl, cpl, std::min(4, ceil_div(rows_guess, kTileWarps)));
+        if (!fn) return false;
+        const size_t smem = tile_smem<T>(rows_guess, sw, cl);
+        if (smem > 200 * 1024) return false;
+        GOAT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cl * num_sms);
+        cfg.blockDim = dim3(kTileThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at;
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = cl; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        GOAT_CUDA(cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg));
+    }
+    if (ncl < 1) return false;
+    const int ngrp = std::max(1, std::min(ncl, n / 2));
+    const int rows_g = (int)round_up(ceil_div(n, ngrp), 2);
+    const int rpw = ceil_div(rows_g, kTileWarps);
+    if (rpw > 4) return false;
+    void *fn = tile_for<T>(cl, cpl, rpw);
+    if (!fn) return false;
+    p.smem = tile_smem<T>(rows_g, sw, cl);
+    if (p.smem > 200 * 1024) return false;
+    GOAT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    p.tile = true;
+    p.persistent = true;
+    p.cl = cl;
+    p.nt = kTileThreads;
+    p.ch = cpl;
+    p.rows = rpw;
+    p.tile_rows = rows_g;
+    p.slice_w = (int)round_up(ceil_div(n, cl), 8);
+    p.ngrp = (n + rows_g - 1) / rows_g;
+    p.nblk = p.ngrp * cl;
+    p.merge_blocks = 1;
+    p.colpart_bytes = (size_t)std::max(p.ngrp, num_sms * 2) * round_up(n, 8) * sizeof(T);
+    return true;
+}
+
+// Small n (whole-LOT-resident tiles, see sk_tile_kernel): clusters of 2 (n < 512)
+// or 4 CTAs split the columns; row groups = co-resident clusters.
+template <class T> bool tile_plan(int n, int num_sms, SkPlan &p) {
+    if (env_int("GOAT_SK_TILE", 1) == 0) return false;
+    const int cl = env_int("GOAT_SK_TILE_CL", n < 512 ? 2 : 4);
+    if (cl != 2 && cl != 4) return false;
+    const int sw = (int)round_up(ceil_div(n, cl), 32);
+    const int cpl = sw / 32;
+    if (cpl != 1 && cpl != 2 && cpl != 4 && cpl != 8 && !(cl == 4 && cpl == 16)) {
+        // round the slice up to the next instantiated width
+        int c = 1;
+        while (c < cpl) c *= 2;
+        if (c > (cl == 4 ? 16 : 8)) return false;
+        return tile_plan_width<T>(n, num_sms, p, cl, c);
+    }
+    return tile_plan_width<T>(n, num_sms, p, cl, cpl);
+}
+
+template <class T> SkPlan sk_plan(int n, int num_sms, int mrows, bool sharded) {
     if (mrows < 0) mrows = n;
     constexpr int VW = VecT<T>::W;
     SkPlan p;
+    if (!sharded && mrows == n && tile_plan<T>(n, num_sms, p)) return p;
     if (sizeof(T) == 4 && ceil_div(ceil_div(n, VW), kThreads) > kMaxCh && env_int("GOAT_SK_PIPE", 1) &&
         pipe_plan(n, mrows, p)) {
         void *const kfn = pipe_for(p.ch, p.cl, p.nt, p.rows);
@@ -2174,8 +2506,12 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
     void *params[] = {&args, &bar};
     cudaLaunchAttribute attrs[2];
     cudaLaunchConfig_t cfg = persistent_config(p, s, attrs);
-    void *fn = p.pipe ? pipe_for(p.ch, p.cl, p.nt, p.rows) : persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
-    GOAT_CUDA(cudaLaunchKernelExC(&cfg, fn, params));
+    if (p.tile && args.single_pass) throw Error(GOAT_ENOTSUP, "sinkhorn: the tile plan has no single-pass mode");
+    void *fn = p.tile ? tile_for<T>(p.cl, p.ch, p.rows)
+                      : p.pipe ? pipe_for(p.ch, p.cl, p.nt, p.rows) : persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
+    int rows_g = p.tile_rows;
+    void *tparams[] = {&args, &bar, &rows_g};
+    GOAT_CUDA(cudaLaunchKernelExC(&cfg, fn, p.tile ? tparams : params));
     note_launch();
 }
 
@@ -2222,8 +2558,8 @@ void sk_launch_emit(const SkArgs &a, T *Q, int64_t ldq, const T *P, int64_t ldp,
     GOAT_CHECK_LAUNCH();
 }
 
-template SkPlan sk_plan<float>(int, int, int);
-template SkPlan sk_plan<double>(int, int, int);
+template SkPlan sk_plan<float>(int, int, int, bool);
+template SkPlan sk_plan<double>(int, int, int, bool);
 template void sk_launch_shard_pass<float>(const SkArgs &, const SkPlan &, unsigned *, double *, cudaStream_t);
 template void sk_launch_shard_pass<double>(const SkArgs &, const SkPlan &, unsigned *, double *, cudaStream_t);
 template void sk_launch_shard_merge<float>(const SkArgs &, const double *, int, unsigned char *, cudaStream_t);
