@@ -2289,6 +2289,7 @@ template <class T> void *tile_for(int cl, int cpl, int rpw) {
     }
     GOAT_TL(2, 1) GOAT_TL(2, 2) GOAT_TL(2, 4) GOAT_TL(2, 8)
     GOAT_TL(4, 1) GOAT_TL(4, 2) GOAT_TL(4, 4) GOAT_TL(4, 8) GOAT_TL(4, 16)
+    GOAT_TL(8, 2) GOAT_TL(8, 4) GOAT_TL(8, 8)
 #undef GOAT_TL
     return nullptr;
 }
@@ -2345,19 +2346,20 @@ template <class T> bool tile_plan_width(int n, int num_sms, SkPlan &p, int cl, i
     return true;
 }
 
-// Small n (whole-LOT-resident tiles, see sk_tile_kernel): clusters of 2 (n < 512)
-// or 4 CTAs split the columns; row groups = co-resident clusters.
+// Small n (whole-LOT-resident tiles, see sk_tile_kernel): clusters of 4 CTAs
+// split the columns; row groups = co-resident clusters.
 template <class T> bool tile_plan(int n, int num_sms, SkPlan &p) {
     if (env_int("GOAT_SK_TILE", 1) == 0) return false;
-    const int cl = env_int("GOAT_SK_TILE_CL", n < 512 ? 2 : 4);
-    if (cl != 2 && cl != 4) return false;
+    // measured: 2 CTAs at n = 64 (3.7 vs 5.7 us), 4 from n = 500 (4.1 vs 6.2 us)
+    const int cl = env_int("GOAT_SK_TILE_CL", n < 256 ? 2 : 4);
+    if (cl != 2 && cl != 4 && cl != 8) return false;
     const int sw = (int)round_up(ceil_div(n, cl), 32);
     const int cpl = sw / 32;
-    if (cpl != 1 && cpl != 2 && cpl != 4 && cpl != 8 && !(cl == 4 && cpl == 16)) {
+    if ((cpl != 1 && cpl != 2 && cpl != 4 && cpl != 8 && !(cl == 4 && cpl == 16)) || (cl == 8 && cpl < 2)) {
         // round the slice up to the next instantiated width
         int c = 1;
         while (c < cpl) c *= 2;
-        if (c > (cl == 4 ? 16 : 8)) return false;
+        if (c > (cl == 4 ? 16 : 8) || (cl == 8 && c < 2)) return false;
         return tile_plan_width<T>(n, num_sms, p, cl, c);
     }
     return tile_plan_width<T>(n, num_sms, p, cl, cpl);
