@@ -2019,6 +2019,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
     for (int k = k0;; ++k, par ^= 1) {
         const bool pre = (k == 0), rowonly = (k == K + 1);
         double *fout = fslot(a, k);
+        sk_stamp(a, k, 0);
         if (tid == 0) xbar_arm(&xbar[par], (uint32_t)(CL * nr * 2 * sizeof(T)));
         // ---- rows: warp w owns rows w, w + NW, ...
         T y[RPW][CPL], mw[RPW];
@@ -2069,7 +2070,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
                 }
             }
         }
+        sk_stamp_v(a, k, 1, (double)sw[0]);
         xbar_wait(&xbar[par], (uint32_t)((k - k0) >> 1) & 1u);
+        sk_stamp(a, k, 2);
         double devmax = 0.0;
         T sc[RPW];
 #pragma unroll
@@ -2108,7 +2111,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
             }
         }
         if (lane == 0) s_red[warp] = devmax;
+        sk_stamp(a, k, 3);
         __syncthreads();
+        sk_stamp(a, k, 4);
         if (!rowonly) {
             T *cp = static_cast<T *>(a.colpart) + (int64_t)grp * a.ldp;
             for (int c = tid; c < SW; c += kTileThreads) {
@@ -2126,7 +2131,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
             // cleared a full sweep before its next use (see below)
             if (d > 0.0) atomicMax(a.dslot + 3 + (k % 3), (unsigned long long)__double_as_longlong(d));
         }
+        sk_stamp(a, k, 5);
         grid_barrier(bar, gridDim.x, epoch);
+        sk_stamp(a, k, 6);
         const double drow = __longlong_as_double((long long)__ldcg(a.dslot + 3 + (k % 3)));
         int stop = 0, sweeps = 0, conv = 0, slot = 0;
         if (k >= 2) {
@@ -2141,7 +2148,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
             }
             break;
         }
-        // ---- merge of this CTA's columns (fixed order over the row groups, fp64)
+        // ---- merge of this CTA's columns (fixed order over the row groups, fp64).
+        // (Measured: this plain loop beats batching all partial loads or splitting a
+        // column's groups over two threads -- profiles/round1_sk_tile.md.)
         const T *cpa = static_cast<const T *>(a.colpart);
         const double tiny = sizeof(T) == 4 ? 1e-30 : 1e-290;
         double dloc = 0.0;
@@ -2161,7 +2170,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
                 if (grp == 0) __stcg(gslot(a, k) + j, gnew);
             }
         }
-        // slot of sweep k+2: last read after the barrier of sweep k-1, next written after barrier k+1
         if (blockIdx.x == 0 && tid == 0) a.dslot[3 + ((k + 2) % 3)] = 0ull;
         if (pre) {
 #pragma unroll
@@ -2185,7 +2193,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
                 break;
             }
         }
+        sk_stamp(a, k, 7);
         __syncthreads();  // the new g slice before the next pass
+        sk_stamp(a, k, 8);
     }
     if constexpr (CL > 1) cluster_sync();  // no CTA leaves while peers may still write into it
 }
