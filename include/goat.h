@@ -101,6 +101,16 @@ int goat_fw_core(goat_handle *h, int64_t n,
                  const double *L, int64_t ldl, const double *P0, int64_t ldp,
                  const goat_options *opts, goat_fw_result *res);
 
+/* Seeded _fw_core (matcher.py:245-269): the free blocks A22, B22 (nf x nf) and the
+ * seed blocks A21, B21 (nf x m), A12, B12 (m x nf) of the seed-reordered,
+ * shuffled inputs; the constant linear term L = A21 B21^T + A12^T B12
+ * (matcher.py:267) is formed on the device.  objective = the free-block terms. */
+int goat_fw_core_seeded(goat_handle *h, int64_t nf, int64_t m,
+                        const double *A22, int64_t lda22, const double *B22, int64_t ldb22,
+                        const double *A21, int64_t lda21, const double *A12, int64_t lda12,
+                        const double *B21, int64_t ldb21, const double *B12, int64_t ldb12,
+                        const double *P0, int64_t ldp, const goat_options *opts, goat_fw_result *res);
+
 /* Same, inputs already resident on the handle's device (row-major, element
  * type = the handle's precision: float for GOAT_FP32, double for GOAT_FP64). */
 int goat_fw_core_device(goat_handle *h, int64_t n,

@@ -81,6 +81,8 @@ def _bind(lib):
                                                    ctypes.POINTER(GoatCsr), ctypes.c_void_p, ctypes.c_int64,
                                                    ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(GoatOptions),
                                                    ctypes.POINTER(GoatFwResult)]),
+        "goat_fw_core_seeded": (ctypes.c_int, [H, ctypes.c_int64, ctypes.c_int64] + [_c_double_p, ctypes.c_int64] * 7
+                                + [ctypes.POINTER(GoatOptions), ctypes.POINTER(GoatFwResult)]),
         "goat_gradient_csr": (ctypes.c_int, [H, ctypes.c_int64, ctypes.POINTER(GoatCsr), ctypes.POINTER(GoatCsr),
                                              _c_double_p, ctypes.c_int64, _c_double_p, ctypes.c_int64]),
         "goat_bench_gradient_csr": (ctypes.c_int, [H, ctypes.c_int64, ctypes.POINTER(GoatCsr),
@@ -144,7 +146,7 @@ def _bind(lib):
 
 #: Every symbol include/goat.h declares (checked by tests/test_abi.py).
 EXPORTS = ("goat_create", "goat_destroy", "goat_last_error", "goat_version", "goat_reserve",
-           "goat_fw_core", "goat_fw_core_device", "goat_fw_core_csr", "goat_fw_core_csr_device",
+           "goat_fw_core", "goat_fw_core_device", "goat_fw_core_seeded", "goat_fw_core_csr", "goat_fw_core_csr_device",
            "goat_gradient_csr", "goat_bench_gradient_csr", "goat_gradient", "goat_lot",
            "goat_sinkhorn_knopp", "goat_line_search_coeffs", "goat_lap",
            "goat_qap_objective_perm", "goat_set_stream", "goat_bench_sweep",

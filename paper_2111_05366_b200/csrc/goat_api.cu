@@ -995,6 +995,64 @@ void fw_core_csr(Handle &h, int64_t n, const goat_csr &A, const goat_csr &B, boo
     res->time_ms[5] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
+
+// ------------------------------------------------------------------ seeded core
+// matcher.py:245-269: with m seeds the free block is matched with the constant
+// linear term L = A21 B21^T + A12^T B12 (matcher.py:267).  The reference forms L
+// on the host (an nf x nf product of inner size m); here the seed blocks cross the
+// boundary and L is formed on the device by two GEMMs.
+template <class T>
+void upload_rect(Ctx &c, const double *src, int64_t lds, int rows, int cols, T *dst, int64_t ldd) {
+    std::vector<T> tmp((size_t)rows * ldd, T(0));
+    for (int r = 0; r < rows; ++r)
+        for (int q = 0; q < cols; ++q) tmp[(size_t)r * ldd + q] = (T)src[(int64_t)r * lds + q];
+    GOAT_CUDA(cudaMemcpyAsync(dst, tmp.data(), tmp.size() * sizeof(T), cudaMemcpyHostToDevice, c.s));
+    GOAT_CUDA(cudaStreamSynchronize(c.s));  // tmp goes out of scope
+}
+
+template <class T>
+void fw_core_seeded(Handle &h, int64_t nf, int64_t m, const double *A22, int64_t lda22, const double *B22,
+                    int64_t ldb22, const double *A21, int64_t lda21, const double *A12, int64_t lda12,
+                    const double *B21, int64_t ldb21, const double *B12, int64_t ldb12, const double *P0,
+                    int64_t ldp, const goat_options *o, goat_fw_result *res) {
+    auto t0 = std::chrono::steady_clock::now();
+    ensure_workspace(h, nf);
+    ensure_f64_inputs(h, nf);
+    h.L.ensure(h.A.bytes);
+    h.Gl.ensure(h.A.bytes);
+    Ctx c(h, (int)nf);
+    Timer setup(c.s);
+    upload<T>(c, A22, lda22, h.A.as<T>(), h.A64.as<double>());
+    upload<T>(c, B22, ldb22, h.B.as<T>(), h.B64.as<double>());
+    if (P0) upload<T>(c, P0, ldp, h.P.as<T>(), h.stage.as<double>());
+    // seed blocks: [A21 | B21] (nf x m) and [A12 | B12] (m x nf), leading dim ldm / c.ld
+    const int64_t ldm = round_up(std::max<int64_t>(m, 1), 8);
+    DevBuf blk;
+    blk.ensure(((size_t)2 * nf * ldm + (size_t)2 * m * c.ld) * sizeof(T));
+    T *a21 = blk.as<T>(), *b21 = a21 + nf * ldm, *a12 = b21 + nf * ldm, *b12 = a12 + m * c.ld;
+    upload_rect<T>(c, A21, lda21, (int)nf, (int)m, a21, ldm);
+    upload_rect<T>(c, B21, ldb21, (int)nf, (int)m, b21, ldm);
+    upload_rect<T>(c, A12, lda12, (int)m, (int)nf, a12, c.ld);
+    upload_rect<T>(c, B12, ldb12, (int)m, (int)nf, b12, c.ld);
+    T *L = h.L.as<T>();
+    GOAT_CUDA(cudaMemsetAsync(L, 0, h.L.bytes, c.s));
+    gemm_simt<T>((int)nf, (int)nf, (int)m, 1.0, a21, ldm, 0, b21, ldm, 1, 0.0, L, c.ld, c.s);  // A21 B21^T
+    gemm_simt<T>((int)nf, (int)nf, (int)m, 1.0, a12, c.ld, 1, b12, c.ld, 0, 1.0, L, c.ld, c.s);  // + A12^T B12
+    res->time_ms[4] = setup.stop();
+    fw_loop<T>(c, true, P0 == nullptr, *o, res);
+    // objective on the free block (the caller adds the seed terms, matcher.py:283)
+    int *perm = h.ivec.as<int>();
+    std::vector<int> ph(nf);
+    for (int64_t r = 0; r < nf; ++r) ph[r] = (int)res->assignment[r];
+    GOAT_CUDA(cudaMemcpyAsync(perm, ph.data(), nf * 4, cudaMemcpyHostToDevice, c.s));
+    launch_qap_perm(h.A64.as<double>(), c.ld, h.B64.as<double>(), c.ld, perm, (int)nf, h.red.as<double>(),
+                    h.scal.as<double>() + 40, c.s);
+    GOAT_CUDA(cudaMemcpyAsync(h.h_scal + 40, h.scal.as<double>() + 40, 8, cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    res->objective = h.h_scal[40];
+    res->time_ms[5] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
 template <class T> SkArgs shard_sk_args(Handle &h, const void *G) {
     auto &S = h.sh;
     SkArgs a{};
@@ -1778,6 +1836,29 @@ int goat_bench_gradient_csr(goat_handle *h, int64_t n, const goat_csr *dA, const
                 gradient<T>(c, (const T *)nullptr, (const T *)nullptr, h->P.as<T>(), h->G.as<T>(), h->T1.as<T>());
             *ms = tm.stop() / reps;
         });
+    });
+}
+
+
+int goat_fw_core_seeded(goat_handle *h, int64_t nf, int64_t m, const double *A22, int64_t lda22, const double *B22,
+                        int64_t ldb22, const double *A21, int64_t lda21, const double *A12, int64_t lda12,
+                        const double *B21, int64_t ldb21, const double *B12, int64_t ldb12, const double *P0,
+                        int64_t ldp, const goat_options *opts, goat_fw_result *res) {
+    return guarded([&] {
+        require(h && A22 && B22 && res && res->assignment && res->hist_obj && res->hist_alpha, "NULL argument");
+        require(m >= 1 && A21 && A12 && B21 && B12, "seed blocks must be given (m >= 1)");
+        check_order(nf);
+        validate_opts(opts);
+        require(lda22 >= nf && ldb22 >= nf && lda21 >= m && ldb21 >= m && lda12 >= nf && ldb12 >= nf &&
+                    (!P0 || ldp >= nf),
+                "leading dimension too small");
+        launch_count() = 0;
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            fw_core_seeded<T>(*h, nf, m, A22, lda22, B22, ldb22, A21, lda21, A12, lda12, B21, ldb21, B12, ldb12,
+                              P0, ldp, opts, res);
+        });
+        res->gpu_launches = (int32_t)launch_count();
     });
 }
 

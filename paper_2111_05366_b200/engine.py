@@ -44,6 +44,21 @@ def fw_core(A, B, L, P0, opts: MatchOptions):
         _lib.dptr(P_) if P_ is not None else None, _lib.ld_of(P_) if P_ is not None else n, o, res))
 
 
+def fw_core_seeded(A22, B22, A21, A12, B21, B12, P0, opts: MatchOptions):
+    """``fw_core`` with the seed term formed on the device (goat_fw_core_seeded):
+    L = A21 B21^T + A12^T B12 (matcher.py:267) from the seed blocks."""
+    nf, m = A21.shape
+    h = _lib.handle(opts.device, opts.precision)
+    blocks = [_lib.f64(x) for x in (A22, B22, A21, A12, B21, B12)]
+    P_ = _lib.f64(P0) if P0 is not None else None
+    args = []
+    for b in blocks:
+        args += [_lib.dptr(b), _lib.ld_of(b) if b.shape[0] > 1 else b.shape[1]]
+    return _call_core(nf, opts, h, lambda lib, o, res: lib.goat_fw_core_seeded(
+        h.ptr, nf, m, *args, _lib.dptr(P_) if P_ is not None else None, _lib.ld_of(P_) if P_ is not None else nf,
+        o, res))
+
+
 def _call_core(n, opts: MatchOptions, h, call):
     mi = opts.max_iters
     assign = np.empty(n, dtype=np.int64)
@@ -198,20 +213,30 @@ def _match(A, B, pairs: np.ndarray, opts: MatchOptions) -> MatchResult:
             B22 = permute_matrix(Br[m:, m:], shuf) if opts.shuffle_input else Br[m:, m:]
         A22 = Ar[m:, m:]
         L = None
+        seed_blocks = None
         if m:
             B12 = Br[:m, m:][:, inv]
             B21 = Br[m:, :m][inv, :]
-            L = Ar[m:, :m] @ B21.T + Ar[:m, m:].T @ B12  # constant seed term (matcher.py:267)
             if sparse:
+                L = Ar[m:, :m] @ B21.T + Ar[:m, m:].T @ B12  # constant seed term (matcher.py:267)
                 L = np.asarray(L.toarray(), dtype=np.float64)
+            else:
+                # formed on the device from the seed blocks (goat_fw_core_seeded)
+                seed_blocks = (Ar[m:, :m], Ar[:m, m:], B21, B12)
         diag = None
         if nf == 1:
             p22 = np.zeros(1, dtype=np.intp)
+            if seed_blocks is not None:  # 1 x 1 seed term on the host (matcher.py:267)
+                L = seed_blocks[0] @ seed_blocks[2].T + seed_blocks[1].T @ seed_blocks[3]
             history, iters, conv = [(0, _quadratic_1x1(A22, B22, L), None)], 0, True
         else:
             P0 = _initial(nf, opts, rng)
-            core = fw_core_csr if sparse else fw_core
-            p22, history, iters, conv, diag = core(A22, B22, L, P0, opts)
+            if seed_blocks is not None:
+                A21, A12, B21_, B12_ = seed_blocks
+                p22, history, iters, conv, diag = fw_core_seeded(A22, B22, A21, A12, B21_, B12_, P0, opts)
+            else:
+                core = fw_core_csr if sparse else fw_core
+                p22, history, iters, conv, diag = core(A22, B22, L, P0, opts)
         p22 = inv[p22]
         align = np.empty(n, dtype=np.intp)
         align[ord1[:m]] = ord2[:m]

@@ -249,3 +249,25 @@ def test_monotone_objective_and_sandwich():
         vals = [gb.qap_objective(A, B, np.array(p)) for p in itertools.permutations(range(5))]
         res = gb.frank_wolfe_match(A, B, gb.MatchOptions(step_solver="lot"))
         assert min(vals) - 1e-9 <= res.objective <= max(vals) + 1e-9
+
+
+@pytest.mark.parametrize("m", [1, 7, 39])
+def test_seeded_device_L_matches_oracle(m):
+    """The seed term L = A21 B21^T + A12^T B12 (matcher.py:267) formed on the device
+    (goat_fw_core_seeded) on weighted directed graphs: the oracle's seeded run,
+    including the m = n - 1 case (a 1 x 1 free block)."""
+    n = 40
+    rng = np.random.default_rng(100 + m)
+    A = (rng.random((n, n)) < 0.3) * rng.lognormal(0, 1, (n, n))
+    B = (rng.random((n, n)) < 0.3) * rng.lognormal(0, 1, (n, n))
+    np.fill_diagonal(A, 0)
+    np.fill_diagonal(B, 0)
+    perm = rng.permutation(n)
+    seeds = np.stack([np.arange(m), perm[:m]], axis=1)
+    opts = gb.MatchOptions(step_solver="lot", precision="fp64", shuffle_input=True, max_iters=12)
+    res = gb.seeded_match(A, B, gb.SeedSet(seeds), opts)
+    align, obj, iters, hist, conv = O.run_seeded(A, B, seeds, shuffle_input=True, max_iters=12)
+    np.testing.assert_array_equal(res.alignment, align)
+    assert res.objective == pytest.approx(obj, rel=1e-12)
+    assert res.iterations == iters and res.converged == conv
+    np.testing.assert_allclose([h[1] for h in res.iterate_history], [h[1] for h in hist], rtol=1e-9)
