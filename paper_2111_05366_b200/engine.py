@@ -168,7 +168,7 @@ def _quadratic_1x1(A22, B22, L):
     return val + (float(L[0, 0]) if L is not None else 0.0)
 
 
-def _match(A, B, pairs: np.ndarray, opts: MatchOptions) -> MatchResult:
+def _match(A, B, pairs: np.ndarray, opts: MatchOptions, group=None) -> MatchResult:
     t0 = time.perf_counter()
     sparse = is_sparse(A) or is_sparse(B)
     if sparse:
@@ -199,8 +199,8 @@ def _match(A, B, pairs: np.ndarray, opts: MatchOptions) -> MatchResult:
         Ar = A[np.ix_(ord1, ord1)] if m else A
         Br = B[np.ix_(ord2, ord2)] if m else B
     nf = n - m
-    best = None
-    for r in range(opts.n_restarts):
+
+    def restart(r):
         rng = np.random.default_rng([opts.rng_seed, r])
         if opts.shuffle_input and nf > 1:
             shuf = rng.permutation(nf).astype(np.intp)
@@ -248,18 +248,50 @@ def _match(A, B, pairs: np.ndarray, opts: MatchOptions) -> MatchResult:
             obj = float(A.multiply(B[align][:, align]).sum())  # core.py:120-124 on the CSR inputs
         else:
             obj = qap_objective(A, B, align, device=opts.device)
+        return align, obj, iters, history, conv, diag
+
+    # restarts are independent (matcher.py:254-285): with a process group each
+    # rank runs restarts r = rank, rank + world, ... on its own GPU and the
+    # results are gathered; the choice below is the reference's, in restart order
+    if group is not None and _dist_world(group) > 1:
+        results = _gather_restarts(restart, opts.n_restarts, group)
+    else:
+        results = [restart(r) for r in range(opts.n_restarts)]
+    best = None
+    for res_r in results:
+        obj = res_r[1]
         if best is None or (obj > best[1] if opts.objective_sense == "maximize" else obj < best[1]):
-            best = (align, obj, iters, history, conv, diag)
+            best = res_r
     align, obj, iters, history, conv, diag = best
     return MatchResult(alignment=align, objective=obj, iterations=iters, iterate_history=history,
                        converged=conv, wall_time=time.perf_counter() - t0, diagnostics=diag)
 
 
-def frank_wolfe_match(A, B, opts: MatchOptions = MatchOptions()) -> MatchResult:
-    """Match two equal-order graphs; FAQ or GOAT depending on ``opts.step_solver``."""
-    return _match(A, B, np.empty((0, 2), dtype=np.intp), opts)
+def _dist_world(group):
+    import torch.distributed as dist
+    return dist.get_world_size(group)
 
 
-def seeded_match(A, B, seeds: SeedSet, opts: MatchOptions = MatchOptions()) -> MatchResult:
+def _gather_restarts(restart, n_restarts, group):
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    mine = {r: restart(r) for r in range(rank, n_restarts, world)}
+    allres = [None] * world
+    dist.all_gather_object(allres, mine, group=group)
+    merged = {}
+    for d in allres:
+        merged.update(d)
+    return [merged[r] for r in range(n_restarts)]
+
+
+def frank_wolfe_match(A, B, opts: MatchOptions = MatchOptions(), *, group=None) -> MatchResult:
+    """Match two equal-order graphs; FAQ or GOAT depending on ``opts.step_solver``.
+    ``group`` (a torch.distributed process group, one rank per GPU) spreads the
+    ``n_restarts`` independent restarts over the ranks; every rank returns the
+    same result as the sequential loop."""
+    return _match(A, B, np.empty((0, 2), dtype=np.intp), opts, group)
+
+
+def seeded_match(A, B, seeds: SeedSet, opts: MatchOptions = MatchOptions(), *, group=None) -> MatchResult:
     """Match with seed pairs pinned; Frank-Wolfe over the free block only."""
-    return _match(A, B, seeds.pairs, opts)
+    return _match(A, B, seeds.pairs, opts, group)
