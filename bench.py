@@ -264,6 +264,12 @@ def run_ours(args):
     achieved = bytes_per_sweep / (msw * 1e-3) / 1e9
     peak, peak_kind = _peaks()
     kernels = _kernel_scan(lib, h, dev, peak)
+    traffic = None
+    try:  # measured DRAM bytes per sweep of this kernel (one ncu --set full capture)
+        with open(os.path.join(ROOT, "profiles", "round1_ncu_traffic.json")) as f:
+            traffic = json.load(f)["sk_tile_kernel_n1000_fp32"]["bytes_per_sweep"]
+    except Exception:
+        traffic = None
 
     if world > 1:
         t = torch.tensor([total_ms, float(iters), sum(e2e_ms), float(e2e_iters)], dtype=torch.float64, device=dev)
@@ -298,7 +304,7 @@ def run_ours(args):
                 "time_to_converge_ms": e2e_max / args.steps},
         "roofline": {"kernel": "sk_tile_kernel (persistent log-domain Sinkhorn LOT, one read of G per sweep)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_kind": peak_kind, "traffic": None,
+                     "peak_kind": peak_kind, "traffic": traffic,
                      "note": f"{bytes_per_sweep} algorithmic bytes per sweep (n^2 fp32, one read of G), "
                              f"{msw * 1000:.2f} us per sweep; at n=1000 the G tiles stay in shared memory "
                              f"for the whole LOT, so the sweep is latency-bound (one grid barrier, one "
