@@ -340,6 +340,37 @@ __global__ void lap_auction_repair(const T *M, AucArgs a, double *u, double *v, 
     }
 }
 
+
+// Warm-start tightening before the repair: a row is kept by the repair only if
+// its auction column attains max_j(val_ij - p_j) exactly.  Bidding leaves the
+// last bidder eps below its second-best column, so many rows miss by < eps.
+// Lowering the price of row i's column by that gap (delta_i) makes the row tight;
+// other rows' maxima may move, so a few Jacobi rounds are run.  Any price vector
+// gives feasible duals (u_i is recomputed as the row max), so exactness is
+// untouched -- this only shrinks the set of rows the repair must re-assign.
+template <class T>
+__global__ void lap_tighten_rows(const T *M, AucArgs a, double *delta) {
+    const int n = a.n, lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int i = gw; i < n; i += nwarps) {
+        const int j0 = a.row_col[i];
+        if (j0 < 0) { if (lane == 0) delta[i] = 0.0; continue; }
+        const T *Mi = M + (int64_t)i * a.ld;
+        double best = -INFINITY;
+        for (int j = lane; j < n; j += 32) best = fmax(best, a.sign * (double)Mi[j] - a.price[j]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
+        if (lane == 0) delta[i] = best - (a.sign * (double)Mi[j0] - a.price[j0]);
+    }
+}
+
+__global__ void lap_tighten_cols(AucArgs a, const double *delta) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+        const int j = a.row_col[i];
+        if (j >= 0 && delta[i] > 0.0) a.price[j] -= delta[i];
+    }
+}
+
 // Drop columns whose row was freed (second pass: col4row is final).
 __global__ void lap_auction_unlink(int n, const int *col4row, int *row4col) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
@@ -544,6 +575,13 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
     void *params[] = {(void *)&M, &a};
     GOAT_CUDA(cudaLaunchCooperativeKernel((const void *)lap_auction_kernel<T>, dim3(grid), dim3(256), params, 0, s));
     note_launch();
+    const char *tr = getenv("GOAT_LAP_TIGHTEN");  // Jacobi rounds (0 = off)
+    const int rounds = tr ? atoi(tr) : 16;  // measured: freed rows 15815 -> 170 at n = 40000, repair 4.3 -> 3.4 s
+    for (int r = 0; r < rounds; ++r) {
+        lap_tighten_rows<T><<<num_sms * 4, 256, 0, s>>>(M, a, aw.row_bid_v);  // row_bid_v: free n-vector now
+        lap_tighten_cols<<<std::max(1, std::min(ceil_div(n, 256), num_sms * 4)), 256, 0, s>>>(a, aw.row_bid_v);
+        note_launch(2);
+    }
     lap_auction_repair<T><<<num_sms * 4, 256, 0, s>>>(M, a, w.u, w.v, w.row4col, w.col4row, aw.counters + 3); note_launch();
     lap_auction_unlink<<<std::max(1, std::min(ceil_div(n, 256), num_sms * 4)), 256, 0, s>>>(n, w.col4row, w.row4col); note_launch();
     GOAT_CHECK_LAUNCH();
