@@ -242,7 +242,49 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
         if (gt == 0) a.counters[0] = 0;
         gbar(a.bar, gridDim.x, epoch);
         for (;;) {
-            // (A) bids of unassigned rows
+            // (A) bids of unassigned rows.  Few bidders (late rounds of a phase): a
+            // whole CTA scans each bidder's row (8x the warps on the row scan);
+            // otherwise a warp per bidder.  Same (best, second, lowest-index) result.
+            if (n - __ldcg(a.counters) <= (int)gridDim.x) {
+                __shared__ double s_w1[8], s_w2[8];
+                __shared__ int s_j1[8];
+                const int wib = threadIdx.x >> 5;
+                for (int i = blockIdx.x; i < n; i += gridDim.x) {
+                    if (__ldcg(a.row_col + i) != -1) continue;  // uniform in the CTA
+                    const T *Mi = M + (int64_t)i * a.ld;
+                    double w1 = -INFINITY, w2 = -INFINITY;
+                    int j1 = INT_MAX;
+                    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+                        const double v = a.sign * (double)Mi[j] - __ldcg(a.price + j);
+                        if (v > w1) { w2 = w1; w1 = v; j1 = j; }
+                        else if (v > w2) w2 = v;
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        const double b1 = __shfl_xor_sync(0xffffffffu, w1, off);
+                        const double b2 = __shfl_xor_sync(0xffffffffu, w2, off);
+                        const int bj = __shfl_xor_sync(0xffffffffu, j1, off);
+                        if (b1 > w1 || (b1 == w1 && bj < j1)) { w2 = fmax(b2, w1); w1 = b1; j1 = bj; }
+                        else w2 = fmax(w2, b1);
+                    }
+                    if (lane == 0) { s_w1[wib] = w1; s_w2[wib] = w2; s_j1[wib] = j1; }
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        for (int q = 1; q < (int)(blockDim.x >> 5); ++q) {
+                            const double b1 = s_w1[q], b2 = s_w2[q];
+                            const int bj = s_j1[q];
+                            if (b1 > w1 || (b1 == w1 && bj < j1)) { w2 = fmax(b2, w1); w1 = b1; j1 = bj; }
+                            else w2 = fmax(w2, b1);
+                        }
+                        const double gap = (w2 == -INFINITY) ? 0.0 : (w1 - w2);
+                        const double bid = __ldcg(a.price + j1) + gap + eps;
+                        a.row_bid[i] = j1;
+                        a.row_bid_v[i] = bid;
+                        atomicMax(a.bid_val + j1, (unsigned long long)__double_as_longlong(bid));
+                    }
+                    __syncthreads();
+                }
+            } else
             for (int i = gw; i < n; i += nwarps) {
                 if (__ldcg(a.row_col + i) != -1) continue;
                 const T *Mi = M + (int64_t)i * a.ld;
