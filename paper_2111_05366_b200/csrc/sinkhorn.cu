@@ -2380,8 +2380,11 @@ template <class T> SkPlan sk_plan(int n, int num_sms, int mrows, bool sharded) {
     constexpr int VW = VecT<T>::W;
     SkPlan p;
     if (!sharded && mrows == n && tile_plan<T>(n, num_sms, p)) return p;
-    if (sizeof(T) == 4 && ceil_div(ceil_div(n, VW), kThreads) > kMaxCh && env_int("GOAT_SK_PIPE", 1) &&
-        pipe_plan(n, mrows, p)) {
+    // fp32 rows of more than 6144 columns take the bulk-copy pipeline (measured at
+    // n = 8192: 0.084 vs 0.104 ms; at n = 5000 the register kernel wins, 0.043 vs
+    // 0.050); GOAT_SK_PIPE=3 forces it for any n, 0 disables it
+    if (sizeof(T) == 4 && (ceil_div(ceil_div(n, VW), kThreads) > 6 || env_int("GOAT_SK_PIPE", 1) == 3) &&
+        env_int("GOAT_SK_PIPE", 1) && pipe_plan(n, mrows, p)) {
         void *const kfn = pipe_for(p.ch, p.cl, p.nt, p.rows);
         GOAT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
         if (p.cl > 1) GOAT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
