@@ -391,7 +391,7 @@ def _kernel_scan(lib, h, dev, hbm_peak):
     from paper_2111_05366_b200 import _lib
     out = {}
     tf_peak, tf_kind = _bf16_peak()
-    for n in (2000, 5000, 40000):
+    for n in (2000, 5000, 12288, 40000):
         G = torch.rand((n, n), dtype=torch.float32, device=dev) * 100.0
         ms = _ms_per_sweep(lib, h, n, G, reps=200 if n < 10000 else 20)
         gbs = n * n * 4 / (ms * 1e-3) / 1e9
