@@ -1935,7 +1935,10 @@ cudaLaunchConfig_t persistent_config(const SkPlan &p, cudaStream_t s, cudaLaunch
     attrs[0].id = cudaLaunchAttributeCooperative;
     // GOAT_SK_NOCOOP=1 drops the cooperative flag (profilers cannot replay it);
     // the grid is still sized to the co-resident maximum.
-    attrs[0].val.cooperative = env_int("GOAT_SK_NOCOOP", 0) ? 0 : 1;
+    // Under ncu (it sets NV_NSIGHT_INJECTION_TRANSPORT_TYPE) a cooperative cluster launch is
+    // refused at replay; the grid is co-resident-sized either way.
+    static const bool profiled = getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr;
+    attrs[0].val.cooperative = (env_int("GOAT_SK_NOCOOP", 0) || profiled) ? 0 : 1;
     attrs[1].id = cudaLaunchAttributeClusterDimension;
     const int cdim = p.cl;
     attrs[1].val.clusterDim.x = cdim;
@@ -2526,7 +2529,15 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
                       : p.pipe ? pipe_for(p.ch, p.cl, p.nt, p.rows) : persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
     int rows_g = p.tile_rows;
     void *tparams[] = {&args, &bar, &rows_g};
-    GOAT_CUDA(cudaLaunchKernelExC(&cfg, fn, p.tile ? tparams : params));
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, p.tile ? tparams : params);
+    if (e != cudaSuccess && attrs[0].val.cooperative) {
+        // a profiler that replays kernels rejects cooperative cluster launches; the
+        // grid is sized to the co-resident maximum, so launch it plainly
+        (void)cudaGetLastError();
+        attrs[0].val.cooperative = 0;
+        e = cudaLaunchKernelExC(&cfg, fn, p.tile ? tparams : params);
+    }
+    GOAT_CUDA(e);
     note_launch();
 }
 

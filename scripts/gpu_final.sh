@@ -4,6 +4,6 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f_sm
 timeout 1500 python -m pytest tests/ -q -m gpu --timeout 300 -p no:cacheprovider -rf > gpurun_out/f_pytest.log 2>&1; echo "pytest rc=$?"; grep -E "passed|failed|FAILED" gpurun_out/f_pytest.log | tail -5
 timeout 900 python bench.py > gpurun_out/f_bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/f_bench.log | cut -c1-400
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/f_bench_ref.log 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/f_bench_ref.log | cut -c1-300
-GOAT_BENCH_C5=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/f_launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/f_ncu.log 2>&1; echo "ncu rc=$?"
+GOAT_SK_NOCOOP=1 GOAT_BENCH_C5=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/f_launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/f_ncu.log 2>&1; echo "ncu rc=$?"
 timeout 600 python scripts/run_configs.py 1,4,3 > gpurun_out/f_configs.log 2>&1; echo "configs rc=$?"; cut -c1-400 gpurun_out/f_configs.log
 GOAT_LAP_CLUSTER=2 GOAT_LAP_VERBOSE=1 timeout 600 python scripts/run_configs.py 3 > gpurun_out/f_c3_lapcluster.log 2>&1; echo "c3 cluster rc=$?"; cut -c1-400 gpurun_out/f_c3_lapcluster.log
