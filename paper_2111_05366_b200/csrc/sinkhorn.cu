@@ -1504,7 +1504,7 @@ __device__ __forceinline__ void pass_body_pipe(const SkArgs &a, int k, int max_s
 __device__ __forceinline__ bool env_shift_ok(const SkArgs &a) { return a.resident != 2; }
 
 template <int CH, int CL, int NT, int R>
-__global__ void __launch_bounds__(NT, 1) sk_pipe_kernel(SkArgs a, unsigned *bar) {
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) sk_pipe_kernel(SkArgs a, unsigned *bar) {
     using T = float;
     constexpr int NW = NT / 32;
     __shared__ int s_k, s_done;
@@ -2206,8 +2206,16 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
 }  // namespace
 
 template <int CH, int CL, int R> void *pipe_fn() { return (void *)sk_pipe_kernel<CH, CL, kWideThreads, R>; }
+template <int CH, int CL> void *pipe_fn256() { return (void *)sk_pipe_kernel<CH, CL, 256, 1>; }
 
 void *pipe_for(int ch, int cl, int nt, int rows) {
+    // two 256-thread CTAs per SM (GOAT_SK_PIPE_NT=256)
+    if (nt == 256 && rows == 1) {
+        if (cl == 4 && ch == 5) return pipe_fn256<5, 4>();
+        if (cl == 8 && ch == 5) return pipe_fn256<5, 8>();
+        if (cl == 8 && ch == 4) return pipe_fn256<4, 8>();
+        if (cl == 8 && ch == 3) return pipe_fn256<3, 8>();
+    }
 #define GOAT_PCL(C)                                                 \
     if (nt == kWideThreads && cl == C && rows == 1) {               \
         switch (ch) {                                               \
@@ -2239,6 +2247,21 @@ void *pipe_for(int ch, int cl, int nt, int rows) {
 bool pipe_plan(int n, int mrows, SkPlan &p) {
     constexpr int VW = 4;
     p.nt = kWideThreads;
+    if (env_int("GOAT_SK_PIPE_NT", 512) == 256) {
+        // experimental: 2 CTAs per SM, 8-CTA clusters, ~108 KB of ring per CTA
+        const int cl = env_int("GOAT_SK_PIPE_CL", 8);
+        p.nt = 256; p.cl = cl; p.rows = 1; p.pipe = true;
+        p.slice_w = (int)round_up(ceil_div(n, cl), 8 * VW);
+        p.ch = std::max(3, ceil_div(ceil_div(p.slice_w, VW), p.nt));
+        if (!((cl == 4 && p.ch == 5) || (cl == 8 && p.ch >= 3 && p.ch <= 5))) return false;
+        p.stage_bytes = (int)round_up((size_t)p.slice_w * sizeof(float), 128);
+        const size_t glb = (size_t)p.nt * p.ch * 16;
+        p.stages = std::min(8, (int)((104 * 1024 - glb) / p.stage_bytes));
+        if (p.stages < 4) return false;
+        p.smem = (size_t)p.stages * p.stage_bytes + glb;
+        (void)mrows;
+        return true;
+    }
     p.cl = 1;
     p.slice_w = (int)round_up(n, 8 * VW);
     p.ch = std::max(3, ceil_div(ceil_div(n, VW), p.nt));
