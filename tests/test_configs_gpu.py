@@ -26,3 +26,46 @@ def test_c5_n4000_matches_oracle(precision):
     np.testing.assert_allclose([h[2] for h in hist[1:]], g["alpha"], atol=1e-6)
     if precision == "fp64":
         assert diag["lot_sweeps"] == g["sweeps"].tolist()
+
+
+def test_c5_full_size_csr_properties():
+    """Config 5 at its full size (n = 40000, CSR, fp32; inputs drawn on the GPU with
+    the config-5 law) through the public CSR path.  The oracle cannot run at this
+    size, so the checks are size-independent: a valid permutation, the
+    returned objective equal to an independent O(nnz) host recomputation
+    sum_{(i,j) in A} B[p(i), p(j)], the iteration history consistent with the
+    reported iterations, and a LOT that returns doubly-stochastic-feasible sweeps."""
+    import ctypes
+
+    import scipy.sparse as sp
+    import torch
+
+    from paper_2111_05366_b200 import _lib
+
+    n = 40000
+    dev = torch.device("cuda", 0)
+    (rA, cA), (rB, cB), perm = graphs.sparse_er_pair_csr_device(n, 0.01, 0.9, seed=5, device=dev)
+    sA, sB = _lib.csr_struct_device(rA, cA), _lib.csr_struct_device(rB, cB)
+    h = _lib.handle(0, "fp32")
+    mi = 3
+    assign = np.empty(n, dtype=np.int64)
+    hobj, halpha = np.empty(mi + 1), np.empty(mi + 1)
+    sweeps = np.zeros(mi, dtype=np.int32)
+    res = _lib.GoatFwResult()
+    res.assignment = assign.ctypes.data_as(_lib._c_i64_p)
+    res.hist_obj, res.hist_alpha = _lib.dptr(hobj), _lib.dptr(halpha)
+    res.lot_sweeps = sweeps.ctypes.data_as(_lib._c_i32_p)
+    o = _lib.GoatOptions(max_iters=mi, max_sweeps=1000, sense=_lib.GOAT_MAXIMIZE, step_solver=_lib.GOAT_STEP_LOT,
+                         fw_tol=1e-2, lam=100.0, sk_tol=1e-8)
+    _lib.check(_lib.load().goat_fw_core_csr_device(h.ptr, n, ctypes.byref(sA), ctypes.byref(sB), None, n, None, n,
+                                                   ctypes.byref(o), ctypes.byref(res)))
+    assert np.array_equal(np.sort(assign), np.arange(n))
+    A = sp.csr_matrix((np.ones(cA.numel()), cA.cpu().numpy(), rA.cpu().numpy()), shape=(n, n))
+    B = sp.csr_matrix((np.ones(cB.numel()), cB.cpu().numpy(), rB.cpu().numpy()), shape=(n, n))
+    Ac = A.tocoo()
+    obj = float(np.asarray(B[assign[Ac.row], assign[Ac.col]]).sum())
+    assert res.objective == obj
+    it = int(res.iterations)
+    assert 1 <= it <= mi
+    assert np.all(np.isfinite(hobj[: it + 1]))
+    assert all(1 <= s <= 1000 for s in sweeps[:it])
