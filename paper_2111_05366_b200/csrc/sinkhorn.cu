@@ -2298,7 +2298,8 @@ bool pipe_plan(int n, int mrows, SkPlan &p) {
         }
         if (!found) return false;
     }
-    if (p.cl == 1) p.rows = 1;
+    if (p.cl == 1)  // rows per band, whole-row CTAs: 2 for short rows (4096 < n <= 6144)
+        p.rows = std::max(1, std::min(2, env_int("GOAT_SK_PIPE_R1", (n > 4096 && n <= 6144) ? 2 : 1)));
     p.pipe = true;
     // ring stages (R row slices each) + one more slice for g (scaled)
     p.stage_bytes = p.rows * (int)round_up((size_t)p.slice_w * sizeof(float), 128);
@@ -2405,12 +2406,18 @@ template <class T> SkPlan sk_plan(int n, int num_sms, int mrows, bool sharded) {
     if (mrows < 0) mrows = n;
     constexpr int VW = VecT<T>::W;
     SkPlan p;
-    if (!sharded && mrows == n && tile_plan<T>(n, num_sms, p)) return p;
+    if (!sharded && mrows == n) {
+        SkPlan tp;  // committed only if complete
+        if (tile_plan<T>(n, num_sms, tp)) return tp;
+    }
     // fp32 rows of more than 6144 columns take the bulk-copy pipeline (measured at
     // n = 8192: 0.084 vs 0.104 ms; at n = 5000 the register kernel wins, 0.043 vs
     // 0.050); GOAT_SK_PIPE=3 forces it for any n, 0 disables it
-    if (sizeof(T) == 4 && (ceil_div(ceil_div(n, VW), kThreads) > 6 || env_int("GOAT_SK_PIPE", 1) == 3) &&
-        env_int("GOAT_SK_PIPE", 1) && pipe_plan(n, mrows, p)) {
+    SkPlan pp;  // a pipe plan is committed only if it is complete
+    // (and 4096 < n <= 6144 with 2-row bands: n = 5000 0.0395 vs 0.0425 ms)
+    if (sizeof(T) == 4 && (ceil_div(ceil_div(n, VW), kThreads) > 6 || (n > 4096 && n <= 6144) ||
+                           env_int("GOAT_SK_PIPE", 1) == 3) &&
+        env_int("GOAT_SK_PIPE", 1) && pipe_plan(n, mrows, pp) && (p = pp, true)) {
         void *const kfn = pipe_for(p.ch, p.cl, p.nt, p.rows);
         GOAT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
         if (p.cl > 1) GOAT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
