@@ -44,3 +44,17 @@ def test_fixed_shift_redo_path(n, monkeypatch):
     assert out["3"].sweeps == out["2"].sweeps and out["3"].deviation == out["2"].deviation
     assert np.abs(out["1"].matrix - out["2"].matrix).max() < 1e-5
     assert out["1"].sweeps == out["2"].sweeps
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 33, 127, 255, 257, 511, 1001, 1999])
+@pytest.mark.parametrize("sense", ["maximize", "minimize"])
+def test_lot_small_orders_tile_kernel(n, sense):
+    """Orders served by the shared-memory tile kernel (2- and 4-CTA clusters, ragged
+    last row group and slice), fp64: the oracle's sweep count, flag and iterate."""
+    rng = np.random.default_rng(n + (sense == "minimize"))
+    M = rng.random((n, n)) * rng.integers(1, 50)
+    params = gb.SinkhornParams(max_sweeps=200)
+    res = gb.lot(M, sense, params, precision="fp64")
+    Q, conv, sweeps, dev = O.lot(M, sense, 100.0, 200, 1e-8)
+    assert res.sweeps == sweeps and res.converged == conv
+    assert np.abs(res.matrix - Q).max() < 1e-9
