@@ -286,10 +286,21 @@ void tc_gradient(Ctx &c, const float *X, float *out) {
 
 // Upload a host fp64 matrix (leading dim lds) into dst (precision T, ld).
 template <class T>
-void upload(Ctx &c, const double *src, int64_t lds, T *dst, double *stage64) {
+void upload(Ctx &c, const double *src, int64_t lds, T *dst, double *stage64, int *nonfinite = nullptr) {
     GOAT_CUDA(cudaMemcpy2DAsync(stage64, c.ld * 8, src, lds * 8, (size_t)c.n * 8, c.n,
                                 cudaMemcpyHostToDevice, c.s));
-    launch_convert<T>(stage64, c.ld, dst, c.ld, c.n, 1.0, c.s);  // also zeroes the padding
+    launch_convert<T>(stage64, c.ld, dst, c.ld, c.n, 1.0, c.s, nonfinite);  // also zeroes the padding
+}
+
+// core.py:23-26: a non-finite entry is a ValueError (GOAT_EINVAL), checked on the
+// device while the inputs are converted (flags: [0] A, [1] B, [2] L, [3] P0).
+void require_finite(Ctx &c, int *flags_dev, int count) {
+    int f[4] = {0, 0, 0, 0};
+    GOAT_CUDA(cudaMemcpyAsync(f, flags_dev, sizeof(int) * count, cudaMemcpyDeviceToHost, c.s));
+    GOAT_CUDA(cudaStreamSynchronize(c.s));
+    static const char *names[4] = {"A", "B", "L", "init"};
+    for (int q = 0; q < count; ++q)
+        if (f[q]) throw Error(GOAT_EINVAL, std::string(names[q]) + " contains non-finite entries");
 }
 
 template <class T> void download(Ctx &c, const T *src, double *dst, int64_t ldd, double *stage64) {
@@ -705,10 +716,13 @@ void fw_core_host(Handle &h, int64_t n, const double *A, int64_t lda, const doub
     if (L) { h.L.ensure(h.A.bytes); h.Gl.ensure(h.A.bytes); }
     Ctx c(h, (int)n);
     Timer setup(c.s);
-    upload<T>(c, A, lda, h.A.as<T>(), h.A64.as<double>());
-    upload<T>(c, B, ldb, h.B.as<T>(), h.B64.as<double>());
-    if (L) upload<T>(c, L, ldl, h.L.as<T>(), h.stage.as<double>());
-    if (P0) upload<T>(c, P0, ldp, h.P.as<T>(), h.stage.as<double>());
+    int *fin = h.lap_misc.as<int>() + 8;  // 4 non-finite flags
+    GOAT_CUDA(cudaMemsetAsync(fin, 0, 4 * sizeof(int), c.s));
+    upload<T>(c, A, lda, h.A.as<T>(), h.A64.as<double>(), fin);
+    upload<T>(c, B, ldb, h.B.as<T>(), h.B64.as<double>(), fin + 1);
+    if (L) upload<T>(c, L, ldl, h.L.as<T>(), h.stage.as<double>(), fin + 2);
+    if (P0) upload<T>(c, P0, ldp, h.P.as<T>(), h.stage.as<double>(), fin + 3);
+    require_finite(c, fin, 4);
     res->time_ms[4] = setup.stop();
     fw_loop<T>(c, L != nullptr, P0 == nullptr, *o, res);
     // objective on the inputs (core.py:120-124), fp64, fixed order

@@ -92,9 +92,11 @@ void launch_fw_dots(const T *GP, const T *GQ, const T *P, const T *Q, const T *L
 // out[0] = sum_ij A_ij * B_{p(i)p(j)}  (A, B fp64)
 void launch_qap_perm(const double *A, int64_t lda, const double *B, int64_t ldb,
                      const int *perm, int n, double *part, double *out, cudaStream_t s);
+// dst = scale * src (n x n, padding zeroed); *nonfinite <- 1 if some src entry is
+// not finite (the reference's ValueError check, core.py:25, fused into the upload)
 template <class T>
 void launch_convert(const double *src, int64_t lds, T *dst, int64_t ldd, int n, double scale,
-                    cudaStream_t s);
+                    cudaStream_t s, int *nonfinite = nullptr);
 template <class T>
 void launch_convert_to_f64(const T *src, int64_t lds, double *dst, int64_t ldd, int n,
                            cudaStream_t s);

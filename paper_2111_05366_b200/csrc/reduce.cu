@@ -114,10 +114,15 @@ __global__ void qap_perm_kernel(const double *A, int64_t lda, const double *B, i
 
 template <class T>
 __global__ void convert_kernel(const double *src, int64_t lds, T *dst, int64_t ldd, int n,
-                               double scale) {
+                               double scale, int *nonfinite) {
+    bool bad = false;
     for (int i = blockIdx.x; i < n; i += gridDim.x)
-        for (int j = threadIdx.x; j < ldd; j += kThreads)
-            dst[(int64_t)i * ldd + j] = (j < n) ? (T)(scale * src[(int64_t)i * lds + j]) : T(0);
+        for (int j = threadIdx.x; j < ldd; j += kThreads) {
+            const double x = (j < n) ? src[(int64_t)i * lds + j] : 0.0;
+            bad |= !isfinite(x);
+            dst[(int64_t)i * ldd + j] = (j < n) ? (T)(scale * x) : T(0);
+        }
+    if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) *nonfinite = 1;
 }
 
 template <class T>
@@ -236,8 +241,8 @@ void launch_qap_perm(const double *A, int64_t lda, const double *B, int64_t ldb,
 
 template <class T>
 void launch_convert(const double *src, int64_t lds, T *dst, int64_t ldd, int n, double scale,
-                    cudaStream_t s) {
-    convert_kernel<T><<<std::min(n, 4096), kThreads, 0, s>>>(src, lds, dst, ldd, n, scale); note_launch();
+                    cudaStream_t s, int *nonfinite) {
+    convert_kernel<T><<<std::min(n, 4096), kThreads, 0, s>>>(src, lds, dst, ldd, n, scale, nonfinite); note_launch();
     GOAT_CHECK_LAUNCH();
 }
 
@@ -304,7 +309,7 @@ void launch_neglog(const T *X, int64_t ldx, T *Y, int64_t ldy, int n, int *bad, 
     template void launch_minmax<T>(const T *, int64_t, int, double *, double *, cudaStream_t, int);   \
     template void launch_fw_dots<T>(const T *, const T *, const T *, const T *, const T *, int64_t, int, \
                                     double *, double *, cudaStream_t, int);                          \
-    template void launch_convert<T>(const double *, int64_t, T *, int64_t, int, double, cudaStream_t); \
+    template void launch_convert<T>(const double *, int64_t, T *, int64_t, int, double, cudaStream_t, int *); \
     template void launch_convert_to_f64<T>(const T *, int64_t, double *, int64_t, int, cudaStream_t); \
     template void launch_fill<T>(T *, int64_t, int, double, cudaStream_t, int);                      \
     template void launch_axpby<T>(double, const T *, double, T *, int64_t, int, cudaStream_t, int);  \

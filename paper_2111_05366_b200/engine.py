@@ -177,8 +177,11 @@ def _match(A, B, pairs: np.ndarray, opts: MatchOptions, group=None) -> MatchResu
         A = as_csr(A, "A")
         B = as_csr(B, "B")
     else:
-        A = as_square_matrix(A, "A")
-        B = as_square_matrix(B, "B")
+        # unseeded dense runs of order > 1 go straight to goat_fw_core, which checks
+        # finiteness during the upload (same ValueError); everything else checks here
+        dev_check = pairs.shape[0] == 0 and np.ndim(A) == 2 and np.shape(A)[0] > 1
+        A = as_square_matrix(A, "A", check_finite=not dev_check)
+        B = as_square_matrix(B, "B", check_finite=not dev_check)
     if A.shape != B.shape:
         raise ValueError(f"order mismatch: {A.shape[0]} vs {B.shape[0]}")
     n = A.shape[0]

@@ -17,11 +17,14 @@ from . import _lib
 DS_TOL = 1e-8
 
 
-def as_square_matrix(M, name: str = "matrix") -> np.ndarray:
+def as_square_matrix(M, name: str = "matrix", check_finite: bool = True) -> np.ndarray:
+    """core.py:17-27.  ``check_finite=False`` is for inputs whose finiteness the
+    library checks itself while uploading them (goat_fw_core raises the same
+    ValueError from the device conversion)."""
     M = np.asarray(M, dtype=float)
     if M.ndim != 2 or M.shape[0] != M.shape[1]:
         raise ValueError(f"{name} must be square, got shape {M.shape}")
-    if not np.all(np.isfinite(M)):
+    if check_finite and not np.all(np.isfinite(M)):
         raise ValueError(f"{name} contains non-finite entries")
     return M
 

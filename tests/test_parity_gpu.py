@@ -271,3 +271,16 @@ def test_seeded_device_L_matches_oracle(m):
     assert res.objective == pytest.approx(obj, rel=1e-12)
     assert res.iterations == iters and res.converged == conv
     np.testing.assert_allclose([h[1] for h in res.iterate_history], [h[1] for h in hist], rtol=1e-9)
+
+
+@pytest.mark.parametrize("which", ["A", "B"])
+@pytest.mark.parametrize("bad", [np.inf, -np.inf, np.nan])
+def test_nonfinite_inputs_raise_valueerror(which, bad):
+    """core.py:23-26: non-finite entries are a ValueError (checked on the device
+    during the upload for unseeded dense runs)."""
+    rng = np.random.default_rng(0)
+    A = (rng.random((30, 30)) < 0.3).astype(float)
+    B = A.copy()
+    (A if which == "A" else B)[3, 7] = bad
+    with pytest.raises(ValueError, match=f"{which} contains non-finite entries"):
+        gb.frank_wolfe_match(A, B, gb.MatchOptions(step_solver="lot"))
