@@ -2359,7 +2359,14 @@ template <class T> bool tile_plan_width(int n, int num_sms, SkPlan &p, int cl, i
         GOAT_CUDA(cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg));
     }
     if (ncl < 1) return false;
-    const int ngrp = std::max(1, std::min(ncl, n / 2));
+    int ngrp = std::max(1, std::min(ncl, n / 2));
+    // Row groups: below n = 256 the merge of a column's partials dominates the
+    // sweep and fewer, taller groups win (measured n = 96: 8 groups 4.1 vs 5.1 us
+    // fp64, 3.3 vs 4.3 us fp32; n = 200: 8 groups fp32 4.0 vs 4.8, 16 groups fp64
+    // 5.5 vs 5.9); from n = 296 every co-resident cluster is best
+    // (profiles/round1_sk_tile_grp.json).  GOAT_SK_TILE_GRP overrides the cap.
+    const int grp_cap = env_int("GOAT_SK_TILE_GRP", n < 256 ? ((sizeof(T) == 8 && n > 128) ? 16 : 8) : 0);
+    if (grp_cap > 0) ngrp = std::max(1, std::min(ngrp, grp_cap));
     const int rows_g = (int)round_up(ceil_div(n, ngrp), 2);
     const int rpw = ceil_div(rows_g, kTileWarps);
     if (rpw > 4) return false;
