@@ -25,6 +25,7 @@ struct SkArgs {
     unsigned long long *dslot = nullptr;  // persistent driver: atomicMax dev slots [row k&1 | col]
     int slice_w = 0;    // cluster-split rows: columns per CTA rank
     int resident = 1;   // keep a CTA's single band in registers across sweeps
+    int l2_last = 0;    // wide-row bulk copies carry an L2 evict_last hint (G fits in L2)
     int stages = 0;     // wide rows: shared-memory ring stages (0 = register path)
     unsigned long long *trace = nullptr;  // diagnostics: per-CTA phase timestamps of sweep trace_k
     int trace_k = -1;

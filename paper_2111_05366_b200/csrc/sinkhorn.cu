@@ -668,6 +668,20 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// The same copy with an L2 cache hint (policy from createpolicy): G is re-read
+// every sweep, so when it fits in L2 an evict_last policy keeps it there.
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 struct WideRing {
@@ -1191,7 +1205,9 @@ __device__ __forceinline__ void pipe_produce(const SkArgs &a, const Slice &sl, P
         for (int r = 0; r < nv; ++r) {
             const int row = sl.grp + (lr0 + r) * sl.ngrp;
             const float *src = static_cast<const float *>(a.G) + (int64_t)row * a.ld + sl.c0;
-            bulk_g2s(rg.base + (size_t)s * rg.stage_bytes + (size_t)r * rg.row_bytes, src, rg.copy_bytes, &ps.full[s]);
+            void *dst = rg.base + (size_t)s * rg.stage_bytes + (size_t)r * rg.row_bytes;
+            if (a.l2_last) bulk_g2s_hint(dst, src, rg.copy_bytes, &ps.full[s], l2_evict_last_policy());
+            else bulk_g2s(dst, src, rg.copy_bytes, &ps.full[s]);
         }
         ++rg.issued;
     }
@@ -2556,6 +2572,9 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
     args.nblk = p.ngrp;  // column-partial rows = row groups
     args.slice_w = p.slice_w;
     args.resident = env_int("GOAT_SK_RES", 1);
+    // G re-read by the bulk-copy ring stays in L2 when it fits (GOAT_SK_L2HINT)
+    args.l2_last = p.pipe && env_int("GOAT_SK_L2HINT", 0) &&
+                   (double)a.n * a.ld * sizeof(T) <= env_int("GOAT_SK_L2HINT_MB", 112) * 1048576.0;
     args.stages = p.stages;
     args.stage_bytes = p.stage_bytes;
     void *params[] = {&args, &bar};
