@@ -2249,6 +2249,8 @@ void *pipe_for(int ch, int cl, int nt, int rows) {
             case 5: return pipe_fn<5, C, 2>();                      \
         }                                                           \
     }
+    // 3 rows per band for whole rows of <= 6144 columns (GOAT_SK_PIPE_R1=3)
+    if (nt == kWideThreads && cl == 1 && ch == 3 && rows == 3) return pipe_fn<3, 1, 3>();
     GOAT_PCL(1)
     GOAT_PCL(2)
     GOAT_PCL(4)
@@ -2315,7 +2317,7 @@ bool pipe_plan(int n, int mrows, SkPlan &p) {
         if (!found) return false;
     }
     if (p.cl == 1)  // rows per band, whole-row CTAs: 2 for short rows (4096 < n <= 6144)
-        p.rows = std::max(1, std::min(2, env_int("GOAT_SK_PIPE_R1", (n > 4096 && n <= 6144) ? 2 : 1)));
+        p.rows = std::max(1, std::min(ceil_div(ceil_div(n, VW), p.nt) <= 3 ? 3 : 2, env_int("GOAT_SK_PIPE_R1", (n > 4096 && n <= 6144) ? 2 : 1)));
     p.pipe = true;
     // ring stages (R row slices each) + one more slice for g (scaled)
     p.stage_bytes = p.rows * (int)round_up((size_t)p.slice_w * sizeof(float), 128);
