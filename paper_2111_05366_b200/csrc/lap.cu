@@ -627,8 +627,12 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
     AucArgs a{};
     a.n = n; a.ld = ld; a.sign = (sense == GOAT_MAXIMIZE) ? 1.0 : -1.0;
     a.eps0 = std::max(range, 1e-300) / 4.0;
-    a.eps_min = std::max(range, 1e-300) * 1e-7 / std::max(n, 1);
-    a.theta = 8.0;
+    // GOAT_LAP_EPS_END (final eps = range * 10^-x / n) and GOAT_LAP_THETA (eps
+    // divisor per phase) trade auction rounds against rows left for the exact repair
+    const char *ee = getenv("GOAT_LAP_EPS_END");
+    const char *th = getenv("GOAT_LAP_THETA");
+    a.eps_min = std::max(range, 1e-300) * pow(10.0, -(ee ? atof(ee) : 7.0)) / std::max(n, 1);
+    a.theta = th ? std::max(2.0, atof(th)) : 8.0;
     a.price = aw.price; a.row_col = aw.row_col; a.col_row = aw.col_row; a.bid_val = aw.bid_val;
     a.bid_row = aw.bid_row; a.row_bid = aw.row_bid; a.row_bid_v = aw.row_bid_v; a.bar = aw.bar;
     a.counters = aw.counters; a.max_rounds = 200000;
