@@ -637,7 +637,11 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
     a.bid_row = aw.bid_row; a.row_bid = aw.row_bid; a.row_bid_v = aw.row_bid_v; a.bar = aw.bar;
     a.counters = aw.counters; a.max_rounds = 200000;
     const char *te = getenv("GOAT_LAP_TAIL");  // divisor: tail = n / div (0 = complete every phase)
-    const int div = te ? atoi(te) : 512;
+    // measured (profiles/round1_lap_tail_scan.log): ending a phase at n/128 free rows
+    // cuts the auction's bidding-war tail at n <= 8192 (c4 LAP 44 -> 29 ms, c3 75 ->
+    // 63 ms, the exact repair absorbs the extra rows); n/512 above, where the
+    // cluster repair of a freed row costs more
+    const int div = te ? atoi(te) : (n <= 8192 ? 128 : 512);
     a.tail = div > 0 ? n / div : 0;
     const char *ke = getenv("GOAT_LAP_KEEP");
     a.keep = ke ? atoi(ke) : 0;  // measured: rounds 6556 -> 6482 at n = 40000, no gain; opt-in
