@@ -1,16 +1,32 @@
-"""GOAT iteration benchmark (BASELINE.json metric: outer iterations/s and
-time-to-converge; Sinkhorn HBM GB/s).
+"""GOAT iteration benchmark (BASELINE.json metric: "GOAT outer iters/sec and
+time-to-converge vs n; Sinkhorn HBM GB/s; GEMM TFLOP/s").
 
-One *step* = one complete GOAT solve (``_fw_core``: every outer iteration plus
-the final exact LAP) of the BASELINE config-2 workload -- n=1000 directed
-correlated ER pair, p=0.1, rho=0.8, fp32, barycenter init, maxiter=30 --
-on a seeded synthetic input.  ``value`` = outer iterations per second over the
-timed steps with inputs already resident in HBM (goat_fw_core_device);
-``e2e`` = the same metric through the public API (frank_wolfe_match on pinned
-host float64 arrays, host<->device copies inside the timed region).
+Headline workload = BASELINE config 5, the largest configuration and the one
+the north star names: n = 40000 undirected sparse correlated ER pair (p = 0.01,
+rho = 0.9), seeded ``graphs.config_pair(5, 0)`` (default_rng([5, 0, block])
+per 2000-row block, hidden permutation from default_rng([5, 0])), CSR adjacency,
+fp32 doubly-stochastic iterate (6.4 GB per n x n buffer), barycenter init,
+maxiter = 30, the reference's defaults otherwise (matcher.py:42-50,
+sinkhorn.py:30-32).
 
-Multi-GPU: config 2 does not shard (n=1000 fits L2); N ranks run N independent
-replicas (replicate r = rank), weak scaling, max-over-ranks device time.
+One *step* = one complete GOAT solve (``_fw_core``, matcher.py:177-212: every
+outer iteration of :187-204 plus the final exact LAP of :205-211).
+``value`` = outer iterations per second over the K timed steps (final LAP time
+included in the denominator) with the CSR inputs resident in HBM
+(goat_fw_core_csr_device); ``e2e`` = the same metric through the public API
+``frank_wolfe_match(scipy.sparse A, scipy.sparse B)`` (host CSR -> device copies
+and the result readback inside the timed region).  Inputs are larger than L2
+(one n x n buffer is 6.4 GB), so no L2 flush is needed between steps.
+
+``--gpus N`` (torchrun, one rank per GPU): the row-sharded path
+(``sharded.sharded_fw_core`` on CSR rows, NCCL between ranks), strong scaling
+(the same n = 40000 problem split over N ranks), time = max over ranks.
+
+``--impl reference``: the reference's CPU path cannot run config 5 (one float64
+n x n buffer is 12.8 GB, ~1.3e15 flop per outer iteration); each step times
+bounded live samples of the reference's own float64 numpy/OpenBLAS operations
+on this host's cores and extrapolates (oracle/cpu_model.py),
+labelled ``extrapolated``.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -18,6 +34,7 @@ replicas (replicate r = rank), weak scaling, max-over-ranks device time.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -31,8 +48,10 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG = 2
-WORKLOAD = "c2: n=1000 directed correlated ER p=0.1 rho=0.8, fp32, barycenter init, maxiter=30"
+CONFIG = 5
+N5 = 40000
+WORKLOAD = ("c5: n=40000 undirected sparse correlated ER p=0.01 rho=0.9 (seeded graphs.config_pair(5,0)), "
+            "CSR adjacency, fp32 iterate, barycenter init, maxiter=30, lam=100, 1000 sweeps max")
 METRIC = "goat_outer_iters_per_sec"
 
 
@@ -69,7 +88,7 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             self._sample()
-            self._stop.wait(0.05)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -95,287 +114,13 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def _inputs(replicate):
-    from paper_2111_05366_b200 import graphs
-    A, Bs, truth = graphs.config_pair(CONFIG, replicate)
-    return A, Bs, truth
-
-
-def _opts():
-    import paper_2111_05366_b200 as gb
-    return gb.MatchOptions(step_solver="lot", precision="fp32", max_iters=30)
-
-
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
-
-
-def cpu_baseline(A, B, budget_s=12.0):
-    """The CPU oracle (numpy port of the reference path) on the same input."""
-    from oracle import goat_oracle as O
-    cores = len(os.sched_getaffinity(0))
-    iters = 0
-    t0 = time.perf_counter()
-    solves = 0
-    while True:
-        _, _, it, _, _ = O.run_seeded(A, B, np.empty((0, 2)), step_solver="lot")
-        iters += it
-        solves += 1
-        if time.perf_counter() - t0 > budget_s or solves >= 8:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": iters / dt, "unit": "iter/s", "cores": cores, "kind": "port",
-            "sample": f"{solves} full c2 solves (n=1000, float64 numpy/OpenBLAS + scipy LSAP), "
-                      f"{iters} outer iterations in {dt:.1f}s",
-            "time_to_converge_ms": 1000.0 * dt / solves}
-
-
-def run_reference(args):
-    rank, world, _ = _dist()
-    if rank != 0:
-        return
-    A, B, _ = _inputs(0)
-    from oracle import goat_oracle as O
-    for _ in range(max(0, min(args.warmup, 1))):
-        O.run_seeded(A, B, np.empty((0, 2)), step_solver="lot")
-    iters = 0
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        _, _, it, _, _ = O.run_seeded(A, B, np.empty((0, 2)), step_solver="lot")
-        iters += it
-    dt = time.perf_counter() - t0
-    cores = len(os.sched_getaffinity(0))
-    v = iters / dt
-    line = {"metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000.0 * dt / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": WORKLOAD, "replicates": 1},
-            "cpu_baseline": {"value": v, "unit": "iter/s", "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full c2 solves of the oracle port "
-                                       f"(oracle/goat_oracle.py, float64, all host threads)"},
-            "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-
-    rank, world, local = _dist()
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-
-    import paper_2111_05366_b200 as gb
-    from paper_2111_05366_b200 import _lib
-
-    A, B, truth = _inputs(rank)
-    n = A.shape[0]
-    opts = gb.MatchOptions(step_solver="lot", precision="fp32", max_iters=30, device=local)
-    h = _lib.handle(local, "fp32")
-    lib = _lib.load()
-    stream = torch.cuda.current_stream(dev)
-    _lib.check(lib.goat_set_stream(h.ptr, _lib.stream_handle(stream)))
-
-    dA = torch.from_numpy(A.astype(np.float32)).to(dev)
-    dB = torch.from_numpy(B.astype(np.float32)).to(dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2
-
-    phases = {}
-
-    def device_step():
-        mi = opts.max_iters
-        assign = np.empty(n, dtype=np.int64)
-        hobj = np.empty(mi + 1)
-        halpha = np.empty(mi + 1)
-        sweeps = np.zeros(mi, dtype=np.int32)
-        res = _lib.GoatFwResult()
-        res.assignment = assign.ctypes.data_as(_lib._c_i64_p)
-        res.hist_obj = _lib.dptr(hobj)
-        res.hist_alpha = _lib.dptr(halpha)
-        res.lot_sweeps = sweeps.ctypes.data_as(_lib._c_i32_p)
-        o = _lib.GoatOptions(max_iters=mi, max_sweeps=1000, sense=_lib.GOAT_MAXIMIZE,
-                             step_solver=_lib.GOAT_STEP_LOT, fw_tol=opts.fw_tol, lam=100.0,
-                             sk_tol=1e-8)
-        _lib.check(lib.goat_fw_core_device(h.ptr, n, dA.data_ptr(), n, dB.data_ptr(), n, None, n,
-                                           None, n, o, res))
-        phases.clear()
-        phases.update(zip(("gradient", "lot", "line_search", "lap", "setup", "total"),
-                          [round(x, 3) for x in res.time_ms]))
-        phases["lot_sweeps"] = sweeps[: int(res.iterations)].tolist()
-        return int(res.iterations), int(res.gpu_launches), assign, float(res.objective)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    for _ in range(max(3, args.warmup)):
-        device_step()
-    # ---- timed: device-resident inputs
-    iters = 0
-    launches = 0
-    ms_steps = []
-    with ClockSampler(local) as clocks:
-        barrier()
-        for _ in range(args.steps):
-            flush.zero_()  # evict L2 between steps (inputs are L2-sized)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            it, nl, assign, obj = device_step()
-            e1.record(stream)
-            e1.synchronize()
-            ms_steps.append(e0.elapsed_time(e1))
-            iters += it
-            launches += nl
-        barrier()
-    total_ms = sum(ms_steps)
-    match = float(np.mean(assign == truth))
-
-    # ---- e2e through the public API, pinned host float64 inputs
-    pA = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
-    pB = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
-    pA[:] = A
-    pB[:] = B
-    gb.frank_wolfe_match(pA, pB, opts)  # warm the host path
-    e2e_ms = []
-    e2e_iters = 0
-    barrier()
-    for _ in range(args.steps):
-        flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        r = gb.frank_wolfe_match(pA, pB, opts)
-        e1.record(stream)
-        e1.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
-        e2e_iters += r.iterations
-    barrier()
-
-    # ---- roofline: the fused Sinkhorn sweep kernel (dominant), live CUDA events
-    G = torch.rand((n, n), dtype=torch.float32, device=dev) * 100.0
-    msw = _ms_per_sweep(lib, h, n, G)
-    bytes_per_sweep = n * n * 4
-    achieved = bytes_per_sweep / (msw * 1e-3) / 1e9
-    peak, peak_kind = _peaks()
-    kernels = _kernel_scan(lib, h, dev, peak)
-    traffic = None
-    try:  # measured DRAM bytes per sweep of this kernel (one ncu --set full capture)
-        with open(os.path.join(ROOT, "profiles", "round1_ncu_traffic.json")) as f:
-            traffic = json.load(f)["sk_tile_kernel_n1000_fp32"]["bytes_per_sweep"]
-    except Exception:
-        traffic = None
-
-    if world > 1:
-        t = torch.tensor([total_ms, float(iters), sum(e2e_ms), float(e2e_iters)], dtype=torch.float64, device=dev)
-        allt = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(allt, t)
-        total_max = max(float(x[0]) for x in allt)
-        iters_all = sum(float(x[1]) for x in allt)
-        e2e_max = max(float(x[2]) for x in allt)
-        e2e_iters_all = sum(float(x[3]) for x in allt)
-    else:
-        total_max, iters_all = total_ms, float(iters)
-        e2e_max, e2e_iters_all = sum(e2e_ms), float(e2e_iters)
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-    c5 = _c5_solve(lib, dev) if os.environ.get("GOAT_BENCH_C5", "1") != "0" else None
-    cpu = cpu_baseline(A, B)
-    line = {
-        "metric": METRIC, "value": iters_all / (total_max / 1000.0), "unit": "iter/s",
-        "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
-        "ms_per_step": total_max / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": n, "replicates_per_gpu": 1,
-                   "l2": "flushed between steps (256 MiB write); inputs 4 MB are L2-sized",
-                   "iterations_per_step": iters / args.steps, "match_ratio": match,
-                   "time_to_converge_ms": total_max / args.steps,
-                   "phase_ms_last_step": phases,
-                   "parallelism": f"replicas x{world}"},
-        "e2e": {"value": e2e_iters_all / (e2e_max / 1000.0), "unit": "iter/s",
-                "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * 8 + 8 * 2 * 31,
-                "time_to_converge_ms": e2e_max / args.steps},
-        "roofline": {"kernel": "sk_tile_kernel (persistent log-domain Sinkhorn LOT, one read of G per sweep)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_kind": peak_kind, "traffic": traffic,
-                     "note": f"{bytes_per_sweep} algorithmic bytes per sweep (n^2 fp32, one read of G), "
-                             f"{msw * 1000:.2f} us per sweep; at n=1000 the G tiles stay in shared memory "
-                             f"for the whole LOT, so the sweep is latency-bound (one grid barrier, one "
-                             f"DSMEM row exchange, one L2 column merge), not HBM-bound"},
-        "cpu_baseline": {k: v for k, v in cpu.items()},
-        "kernels": kernels,
-        "c5": c5,
-        "clocks": clocks.summary(),
-        "gpu_launches": launches,
-    }
-    print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-
-
-def _c5_solve(lib, dev):
-    """BASELINE config 5 (n = 40000 sparse correlated ER, p = 0.01, rho = 0.9, fp32,
-    maxiter = 30) on this GPU through the CSR path: one full solve, inputs drawn on
-    the device (graphs.sparse_er_pair_csr_device).  The north star's target is the
-    outer-iteration time at this size; reported beside the c2 headline."""
-    import ctypes
-    import torch
-    from paper_2111_05366_b200 import _lib, graphs
-    n = 40000
-    (rA, cA), (rB, cB), perm = graphs.sparse_er_pair_csr_device(n, 0.01, 0.9, seed=5, device=dev)
-    sA, sB = _lib.csr_struct_device(rA, cA), _lib.csr_struct_device(rB, cB)
-    h = _lib.handle(dev.index, "fp32")
-    _lib.check(lib.goat_set_stream(h.ptr, _lib.stream_handle(torch.cuda.current_stream(dev))))
-    mi = 30
-    assign = np.empty(n, dtype=np.int64)
-    hobj, halpha = np.empty(mi + 1), np.empty(mi + 1)
-    sweeps = np.zeros(mi, dtype=np.int32)
-    res = _lib.GoatFwResult()
-    res.assignment = assign.ctypes.data_as(_lib._c_i64_p)
-    res.hist_obj, res.hist_alpha = _lib.dptr(hobj), _lib.dptr(halpha)
-    res.lot_sweeps = sweeps.ctypes.data_as(_lib._c_i32_p)
-    o = _lib.GoatOptions(max_iters=mi, max_sweeps=1000, sense=_lib.GOAT_MAXIMIZE,
-                         step_solver=_lib.GOAT_STEP_LOT, fw_tol=1e-2, lam=100.0, sk_tol=1e-8)
-    torch.cuda.synchronize(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    _lib.check(lib.goat_fw_core_csr_device(h.ptr, n, ctypes.byref(sA), ctypes.byref(sB), None, n, None, n,
-                                           ctypes.byref(o), ctypes.byref(res)))
-    e1.record()
-    e1.synchronize()
-    it = int(res.iterations)
-    ph = dict(zip(("gradient", "lot", "line_search", "lap", "setup", "total"), [round(x, 1) for x in res.time_ms]))
-    truth = perm.cpu().numpy()
-    out = {"workload": "c5: n=40000 sparse correlated ER p=0.01 rho=0.9, CSR adjacency (nnz %d + %d), fp32, "
-                       "barycenter init, maxiter=30, one GPU" % (cA.numel(), cB.numel()),
-           "time_to_converge_ms": e0.elapsed_time(e1), "iterations": it, "converged": bool(res.converged),
-           "outer_iteration_ms": (ph["gradient"] + ph["lot"] + ph["line_search"]) / max(1, it),
-           "phase_ms": ph, "lot_sweeps": sweeps[:it].tolist(), "objective": float(res.objective),
-           "match_ratio": max(float(np.mean(assign == truth)), float(np.mean(truth[assign] == np.arange(n)))),
-           "gpu_launches": int(res.gpu_launches)}
-    del rA, cA, rB, cB
-    torch.cuda.empty_cache()
-    return out
-
-
-def _ms_per_sweep(lib, h, n, G, reps=200):
-    import ctypes
-    from paper_2111_05366_b200 import _lib
-    out = ctypes.c_double()
-    _lib.check(lib.goat_bench_sweep(h.ptr, n, G.data_ptr(), n, reps, ctypes.byref(out)))
-    return out.value
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def _bf16_peak():
@@ -387,17 +132,99 @@ def _bf16_peak():
         return 1590.0, "fallback"
 
 
+def _c5_inputs():
+    """Seeded config-5 pair (host generator, the SURVEY §8d convention)."""
+    from paper_2111_05366_b200 import graphs
+    t0 = time.perf_counter()
+    A, Bs, truth = graphs.config_pair(CONFIG, 0)
+    return A, Bs, truth, time.perf_counter() - t0
+
+
+def _to_scipy(g):
+    import scipy.sparse as sp
+    return sp.csr_matrix((np.ones(g.indices.size), g.indices, g.indptr), shape=(g.n, g.n))
+
+
+def _csr_bytes(g):
+    return (g.n + 1) * 8 + g.indices.size * 4
+
+
+def _opts(max_iters=30):
+    from paper_2111_05366_b200 import _lib
+    return _lib.GoatOptions(max_iters=max_iters, max_sweeps=1000, sense=_lib.GOAT_MAXIMIZE,
+                            step_solver=_lib.GOAT_STEP_LOT, fw_tol=1e-2, lam=100.0, sk_tol=1e-8)
+
+
+class DeviceCsrSolver:
+    """goat_fw_core_csr_device on CSR inputs already resident in HBM."""
+
+    def __init__(self, lib, h, g_a, g_b, dev, precision="fp32"):
+        import torch
+        self.lib, self.h, self.n = lib, h, g_a.n
+        self.keep = []
+        self.structs = []
+        for g in (g_a, g_b):
+            rp = torch.from_numpy(np.ascontiguousarray(g.indptr, dtype=np.int64)).to(dev)
+            ci = torch.from_numpy(np.ascontiguousarray(g.indices, dtype=np.int32)).to(dev)
+            self.keep += [rp, ci]
+            from paper_2111_05366_b200 import _lib
+            self.structs.append(_lib.csr_struct_device(rp, ci))
+
+    def solve(self, max_iters=30):
+        from paper_2111_05366_b200 import _lib
+        n, mi = self.n, max_iters
+        self.assign = np.empty(n, dtype=np.int64)
+        hobj, halpha = np.empty(mi + 1), np.empty(mi + 1)
+        sweeps = np.zeros(mi, dtype=np.int32)
+        res = _lib.GoatFwResult()
+        res.assignment = self.assign.ctypes.data_as(_lib._c_i64_p)
+        res.hist_obj, res.hist_alpha = _lib.dptr(hobj), _lib.dptr(halpha)
+        res.lot_sweeps = sweeps.ctypes.data_as(_lib._c_i32_p)
+        o = _opts(mi)
+        _lib.check(self.lib.goat_fw_core_csr_device(self.h.ptr, n, ctypes.byref(self.structs[0]),
+                                                    ctypes.byref(self.structs[1]), None, n, None, n,
+                                                    ctypes.byref(o), ctypes.byref(res)))
+        it = int(res.iterations)
+        self.phases = dict(zip(("gradient", "lot", "line_search", "lap", "setup", "total"),
+                               [round(x, 2) for x in res.time_ms]))
+        self.sweeps = sweeps[:it].tolist()
+        self.alphas = halpha[1:it + 1].tolist()
+        self.objective = float(res.objective)
+        self.converged = bool(res.converged)
+        return it, int(res.gpu_launches)
+
+
+def _ms_per_sweep(lib, h, n, G, reps=200):
+    from paper_2111_05366_b200 import _lib
+    out = ctypes.c_double()
+    _lib.check(lib.goat_bench_sweep(h.ptr, n, G.data_ptr(), n, reps, ctypes.byref(out)))
+    return out.value
+
+
+def _traffic(key):
+    """DRAM bytes per sweep of the dominant kernel from the committed ncu --set full
+    capture (profiles/), per launch like `achieved`; None when not captured."""
+    for name in ("round2_ncu_traffic.json", "round1_ncu_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                d = json.load(f)
+            if key in d:
+                return d[key]["bytes_per_sweep"], name
+        except Exception:
+            pass
+    return None, None
+
+
 def _kernel_scan(lib, h, dev, hbm_peak):
     """Per-kernel rates at the other BASELINE sizes (context for the metric's
     'Sinkhorn HBM GB/s; GEMM TFLOP/s' parts; not the headline)."""
-    import ctypes
     import torch
     from paper_2111_05366_b200 import _lib
     out = {}
     tf_peak, tf_kind = _bf16_peak()
-    for n in (2000, 5000, 12288, 40000):
+    for n in (1000, 2000, 5000, 12288):
         G = torch.rand((n, n), dtype=torch.float32, device=dev) * 100.0
-        ms = _ms_per_sweep(lib, h, n, G, reps=200 if n < 10000 else 20)
+        ms = _ms_per_sweep(lib, h, n, G, reps=200)
         gbs = n * n * 4 / (ms * 1e-3) / 1e9
         out[f"sinkhorn_sweep_n{n}"] = {"us": ms * 1e3, "GB_s": gbs, "frac_hbm": gbs / hbm_peak,
                                        "bytes": n * n * 4}
@@ -425,10 +252,269 @@ def _kernel_scan(lib, h, dev, hbm_peak):
     return out
 
 
+def _dense_config(cfg, precision, dev_index, steps=2):
+    """Secondary: a dense BASELINE config solved through the public API (c2/c3)."""
+    import paper_2111_05366_b200 as gb
+    from paper_2111_05366_b200 import graphs
+    A, B, truth = graphs.config_pair(cfg, 0)
+    opts = gb.MatchOptions(step_solver="lot", precision=precision, device=dev_index)
+    gb.frank_wolfe_match(A, B, opts)  # warm (module load, workspace)
+    best = None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        r = gb.frank_wolfe_match(A, B, opts)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    d = r.diagnostics
+    out = {"precision": precision, "n": A.shape[0], "solve_ms": 1000 * best, "iterations": r.iterations,
+           "outer_iters_per_sec": r.iterations / best, "objective": r.objective,
+           "lot_sweeps": d["lot_sweeps"], "phase_ms": {k: round(v, 2) for k, v in d["time_ms"].items()},
+           "match_ratio": float(np.mean(r.alignment == truth))}
+    gold = os.path.join(ROOT, "tests", "golden", "full_cases.npz")
+    if cfg in (3, 4) and os.path.exists(gold):
+        z = np.load(gold)
+        out["reference_objective"] = float(z[f"c{cfg}_full/objective"])
+        out["same_permutation_as_reference"] = bool(np.array_equal(r.alignment, z[f"c{cfg}_full/alignment"]))
+    return out
+
+
+def cpu_baseline(sweeps_per_iter):
+    """The reference's float64 CPU path at config 5, extrapolated from live anchors
+    on this host (oracle/cpu_model.py), with the model checked on a live c2 solve."""
+    from oracle import cpu_model as CM
+    t0 = time.perf_counter()
+    a = CM.anchors(n=N5)
+    t_it, parts = CM.iteration_seconds(N5, sweeps_per_iter, a)
+    val = CM.validate(a, config=2, max_solves=1)
+    return {"value": 1.0 / t_it, "unit": "iter/s", "cores": CM.host_cores(), "kind": "port",
+            "extrapolated": True,
+            "sample": (f"live float64 numpy/OpenBLAS anchors on this host: dgemm {a['gemm_gflops']:.0f} GFLOP/s "
+                       f"({a['gemm_order']}^3), two-gemv Sinkhorn sweep {a['sweep_s_at_n'] * 1e3:.0f} ms at n=40000 "
+                       f"(timed on a {a['band']}x40000 slab), elementwise {a['elem_gbs']:.1f} GB/s; "
+                       f"extrapolated per-iteration time {t_it:.0f} s at n=40000 with {sweeps_per_iter} sweeps "
+                       f"(final LAP excluded); model / live oracle at c2 = {val['model_over_measured']:.2f}"),
+            "iteration_seconds": t_it, "parts_seconds": parts, "anchors": a, "validation_c2": val,
+            "sample_wall_s": time.perf_counter() - t0}
+
+
+def run_reference(args):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return  # rank 0 alone times the CPU path; the others exit without work
+    from oracle import cpu_model as CM
+    sweeps = 1000  # every config-5 LOT runs the full 1000 sweeps (fp32 and fp64 runs, profiles/)
+    for _ in range(max(1, args.warmup)):
+        a = CM.anchors(n=N5, reps=1)
+    vals, walls = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        a = CM.anchors(n=N5, reps=1)
+        t_it, parts = CM.iteration_seconds(N5, sweeps, a)
+        walls.append(time.perf_counter() - t0)
+        vals.append(1.0 / t_it)
+    v = statistics.median(vals)
+    val = CM.validate(a, config=2, max_solves=1)
+    cores = CM.host_cores()
+    line = {"metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "extrapolated": True,
+            "config": {"workload": WORKLOAD, "n": N5},
+            "cpu_baseline": {"value": v, "unit": "iter/s", "cores": cores, "kind": "port",
+                             "sample": (f"each step: live float64 numpy/OpenBLAS samples of the reference's "
+                                        f"operations on {cores} host threads (dgemm {a['gemm_order']}^3, a "
+                                        f"{a['band']}x40000 two-gemv Sinkhorn slab, an elementwise pass), "
+                                        f"extrapolated to one n=40000 outer iteration with {sweeps} sweeps "
+                                        f"(oracle/cpu_model.py; final LAP excluded); model/live oracle at "
+                                        f"c2 = {val['model_over_measured']:.2f}"),
+                             "step_wall_s": walls, "parts_seconds": parts, "validation_c2": val},
+            "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    rank, world, local = _dist()
+    if world > 1:
+        return run_sharded(args)
+    import torch
+
+    import paper_2111_05366_b200 as gb
+    from paper_2111_05366_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    A, Bs, truth, gen_s = _c5_inputs()
+    n = A.n
+    h = _lib.handle(local, "fp32")
+    lib = _lib.load()
+    stream = torch.cuda.current_stream(dev)
+    _lib.check(lib.goat_set_stream(h.ptr, _lib.stream_handle(stream)))
+    solver = DeviceCsrSolver(lib, h, A, Bs, dev)
+
+    W = max(3, args.warmup)
+    for _ in range(W):
+        solver.solve()
+    iters, launches, ms_steps = 0, 0, []
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize(dev)
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            it, nl = solver.solve()
+            e1.record(stream)
+            e1.synchronize()
+            ms_steps.append(e0.elapsed_time(e1))
+            iters += it
+            launches += nl
+        torch.cuda.synchronize(dev)
+    total_ms = sum(ms_steps)
+    assign = solver.assign
+    match = max(float(np.mean(assign == truth)), float(np.mean(truth[assign] == np.arange(n))))
+    c5 = {"time_to_converge_ms": statistics.median(ms_steps), "iterations": iters // args.steps,
+          "converged": solver.converged, "lot_sweeps": solver.sweeps, "alphas": solver.alphas,
+          "phase_ms_last_step": solver.phases, "objective": solver.objective, "match_ratio": match,
+          "outer_iteration_ms": (solver.phases["gradient"] + solver.phases["lot"] + solver.phases["line_search"])
+          / max(1, iters // args.steps), "host_generator_s": gen_s}
+    del solver
+    torch.cuda.empty_cache()
+
+    # ---- e2e: the public API on host scipy.sparse CSR inputs
+    sA, sB = _to_scipy(A), _to_scipy(Bs)
+    opts = gb.MatchOptions(step_solver="lot", precision="fp32", device=local)
+    gb.frank_wolfe_match(sA, sB, opts)  # warm the host path
+    e2e_ms, e2e_iters = [], 0
+    torch.cuda.synchronize(dev)
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = gb.frank_wolfe_match(sA, sB, opts)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+        e2e_iters += r.iterations
+    e2e_same = bool(np.array_equal(r.alignment, assign)) and r.objective == c5["objective"]
+    del sA, sB
+
+    # ---- roofline: the fused Sinkhorn sweep at n = 40000 (the dominant kernel), live CUDA events
+    G = torch.rand((n, n), dtype=torch.float32, device=dev) * 100.0
+    msw = _ms_per_sweep(lib, h, n, G, reps=50)
+    del G
+    torch.cuda.empty_cache()
+    bytes_per_sweep = n * n * 4
+    achieved = bytes_per_sweep / (msw * 1e-3) / 1e9
+    peak, peak_kind = _peaks()
+    traffic, traffic_src = _traffic("sk_sweep_n40000_fp32")
+    kernels = _kernel_scan(lib, h, dev, peak)
+    secondary = {}
+    if os.environ.get("GOAT_BENCH_SECONDARY", "1") != "0":
+        secondary["c2_fp32"] = _dense_config(2, "fp32", local)
+        secondary["c2_fp64"] = _dense_config(2, "fp64", local)
+        secondary["c3_fp64"] = _dense_config(3, "fp64", local, steps=1)
+        secondary["c3_fp32"] = _dense_config(3, "fp32", local, steps=1)
+    cpu = cpu_baseline(max(c5["lot_sweeps"]) if c5["lot_sweeps"] else 1000)
+
+    line = {
+        "metric": METRIC, "value": iters / (total_ms / 1000.0), "unit": "iter/s",
+        "n_gpus": world, "steps": args.steps, "warmup": W,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": n, "nnz_A": int(A.indices.size), "nnz_B": int(Bs.indices.size),
+                   "l2": "inputs larger than L2 (6.4 GB per n x n fp32 buffer); no flush",
+                   "parallelism": "single GPU", "c5": c5},
+        "e2e": {"value": e2e_iters / (sum(e2e_ms) / 1000.0), "unit": "iter/s",
+                "h2d_bytes_per_step": _csr_bytes(A) + _csr_bytes(Bs),
+                "d2h_bytes_per_step": n * 8 + 8 * (2 * 31 + 3 * 30),
+                "time_to_converge_ms": statistics.median(e2e_ms), "same_result_as_device_path": e2e_same,
+                "api": "frank_wolfe_match(scipy.sparse.csr_matrix A, B, MatchOptions(step_solver='lot', "
+                       "precision='fp32'))"},
+        "roofline": {"kernel": "persistent log-domain Sinkhorn LOT sweep at n=40000 (one read of G per sweep)",
+                     "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
+                     "note": f"{bytes_per_sweep} algorithmic bytes per sweep (n^2 fp32, one read of G), "
+                             f"{msw * 1000:.1f} us per sweep averaged over a 52-sweep LOT launch "
+                             f"(CUDA events on the library stream)"},
+        "cpu_baseline": cpu,
+        "kernels": kernels,
+        "secondary": secondary,
+        "clocks": clocks.summary(),
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_sharded(args):
+    """N ranks, one GPU each: the row-sharded GOAT core on config 5's CSR rows."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_05366_b200 import sharded
+
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    A, Bs, truth, _ = _c5_inputs()
+    sA, sB = _to_scipy(A), _to_scipy(Bs)
+    stream = torch.cuda.current_stream(dev)
+    be, comm = sharded.prepare_csr(sA, sB, precision="fp32")
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    W = max(3, args.warmup)
+    for _ in range(W):
+        sharded.sharded_fw_core(be, comm, None, None, None)
+    ms, iters = [], 0
+    with ClockSampler(local) as clocks:
+        barrier()
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = sharded.sharded_fw_core(be, comm, None, None, None)
+            e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            iters += res.iterations
+        barrier()
+    # e2e: host CSR in, permutation out, through sharded_match
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    r2 = sharded.sharded_match(sA, sB, precision="fp32")
+    t1.record(stream)
+    t1.synchronize()
+    e2e_ms = t0.elapsed_time(t1)
+    t = torch.tensor([sum(ms), e2e_ms], dtype=torch.float64, device=dev)
+    allt = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(allt, t)
+    tmax = max(float(x[0]) for x in allt)
+    emax = max(float(x[1]) for x in allt)
+    if rank == 0:
+        n = A.n
+        match = float(np.mean(truth[res.assignment] == np.arange(n)))
+        line = {"metric": METRIC, "value": iters / (tmax / 1000.0), "unit": "iter/s", "n_gpus": world,
+                "steps": args.steps, "warmup": W, "ms_per_step": tmax / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "n": n, "parallelism": f"row-sharded x{world} (NCCL)",
+                           "iterations_per_step": iters / args.steps, "lot_sweeps": res.lot_sweeps,
+                           "collectives_per_step": res.collectives, "match_ratio": match,
+                           "same_result_e2e": bool(np.array_equal(r2.assignment, res.assignment))},
+                "e2e": {"value": r2.iterations / (emax / 1000.0), "unit": "iter/s",
+                        "h2d_bytes_per_step": _csr_bytes(A) + _csr_bytes(Bs), "d2h_bytes_per_step": n * 8},
+                "clocks": clocks.summary(), "gpu_launches": None}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     args = ap.parse_args()

@@ -154,6 +154,12 @@ int goat_lot(goat_handle *h, int64_t n, const double *M, int64_t ldm, int32_t se
              double lam, int32_t max_sweeps, double tol, double *Q, int64_t ldq,
              int32_t *converged, int32_t *sweeps, double *deviation);
 
+/* lot() on a device-resident M (element type = the handle's precision, leading
+ * dimension round_up(n, 8), 16-byte aligned); Q is written on the device. */
+int goat_lot_device(goat_handle *h, int64_t n, const void *dM, int64_t ldm, int32_t sense,
+                    double lam, int32_t max_sweeps, double tol, void *dQ, int64_t ldq,
+                    int32_t *converged, int32_t *sweeps, double *deviation);
+
 /* sinkhorn.py:60-85  sinkhorn_knopp(K, params) on a strictly positive K. */
 int goat_sinkhorn_knopp(goat_handle *h, int64_t n, const double *K, int64_t ldk,
                         int32_t max_sweeps, double tol, double *Q, int64_t ldq,

@@ -94,6 +94,9 @@ def _bind(lib):
         "goat_lot": (ctypes.c_int, [H, ctypes.c_int64, _c_double_p, ctypes.c_int64, ctypes.c_int32,
                                     ctypes.c_double, ctypes.c_int32, ctypes.c_double, _c_double_p,
                                     ctypes.c_int64, _c_i32_p, _c_i32_p, _c_double_p]),
+        "goat_lot_device": (ctypes.c_int, [H, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                           ctypes.c_double, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p,
+                                           ctypes.c_int64, _c_i32_p, _c_i32_p, _c_double_p]),
         "goat_sinkhorn_knopp": (ctypes.c_int, [H, ctypes.c_int64, _c_double_p, ctypes.c_int64,
                                                ctypes.c_int32, ctypes.c_double, _c_double_p,
                                                ctypes.c_int64, _c_i32_p, _c_i32_p, _c_double_p]),
@@ -147,7 +150,7 @@ def _bind(lib):
 #: Every symbol include/goat.h declares (checked by tests/test_abi.py).
 EXPORTS = ("goat_create", "goat_destroy", "goat_last_error", "goat_version", "goat_reserve",
            "goat_fw_core", "goat_fw_core_device", "goat_fw_core_seeded", "goat_fw_core_csr", "goat_fw_core_csr_device",
-           "goat_gradient_csr", "goat_bench_gradient_csr", "goat_gradient", "goat_lot",
+           "goat_gradient_csr", "goat_bench_gradient_csr", "goat_gradient", "goat_lot", "goat_lot_device",
            "goat_sinkhorn_knopp", "goat_line_search_coeffs", "goat_lap",
            "goat_qap_objective_perm", "goat_set_stream", "goat_bench_sweep",
            "goat_bench_gradient", "goat_lap_device", "goat_shard_setup", "goat_shard_setup_csr", "goat_shard_gradient",

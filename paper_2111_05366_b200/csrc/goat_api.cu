@@ -1240,6 +1240,29 @@ int goat_lot(goat_handle *h, int64_t n, const double *M, int64_t ldm, int32_t se
     return lot_common(h, n, M, ldm, sense, lam, max_sweeps, tol, Q, ldq, converged, sweeps, deviation, 0);
 }
 
+int goat_lot_device(goat_handle *h, int64_t n, const void *dM, int64_t ldm, int32_t sense, double lam,
+                    int32_t max_sweeps, double tol, void *dQ, int64_t ldq, int32_t *converged, int32_t *sweeps,
+                    double *deviation) {
+    return guarded([&] {
+        require(h && dM && dQ, "NULL argument");
+        check_order(n);
+        require(sense == GOAT_MINIMIZE || sense == GOAT_MAXIMIZE, "sense must be minimize or maximize");
+        require(lam > 0 && max_sweeps >= 1 && tol > 0, "invalid Sinkhorn parameters");
+        require(ldm == ld_for(n) && ldq == ld_for(n), "lot_device: leading dimensions must be round_up(n, 8)");
+        require(((uintptr_t)dM & 15) == 0 && ((uintptr_t)dQ & 15) == 0, "lot_device: buffers must be 16-byte aligned");
+        ensure_workspace(*h, n, false);
+        dispatch(*h, [&](auto *tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            Ctx c(*h, (int)n);
+            LotOut lo = run_lot<T>(c, static_cast<const T *>(dM), sense, lam, max_sweeps, tol, static_cast<T *>(dQ),
+                                   nullptr, nullptr, 0);
+            if (converged) *converged = lo.converged;
+            if (sweeps) *sweeps = lo.sweeps;
+            if (deviation) *deviation = lo.dev;
+        });
+    });
+}
+
 int goat_sinkhorn_knopp(goat_handle *h, int64_t n, const double *K, int64_t ldk, int32_t max_sweeps, double tol,
                         double *Q, int64_t ldq, int32_t *converged, int32_t *sweeps, double *deviation) {
     return lot_common(h, n, K, ldk, GOAT_MAXIMIZE, 1.0, max_sweeps, tol, Q, ldq, converged, sweeps, deviation, 1);

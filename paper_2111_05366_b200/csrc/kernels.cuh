@@ -48,6 +48,7 @@ struct SkPlan {
     size_t smem = 0;          // dynamic shared memory of the persistent kernel
     bool pipe = false;        // wide fp32 rows: decoupled bulk-copy pipeline (sk_pipe_kernel)
     bool tile = false;        // small n: shared-memory-resident tiles, one barrier per sweep (sk_tile_kernel)
+    bool wide2 = false;       // 12288 < n <= 40960 fp32: 2-CTA clusters, registers hold y and the column sums (sk_wide_kernel)
     int tile_rows = 0;        // rows per row group of the tile kernel
 };
 

@@ -242,6 +242,9 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
         // every row that already satisfies eps-complementary slackness for the new
         // eps (its column within eps of its best profit) and free only the others,
         // so a phase re-bids the violators instead of all n rows.
+        // Every CTA has read counters[0] for the previous phase's stop test
+        // before it is reset (a slow CTA would otherwise see 0 and keep bidding).
+        if (rounds > 0) gbar(a.bar, gridDim.x, epoch);
         if (rounds == 0 || a.keep == 0) {
             for (int j = gt; j < n; j += nt) { a.row_col[j] = -1; a.col_row[j] = -1; }
             if (gt == 0) a.counters[0] = 0;

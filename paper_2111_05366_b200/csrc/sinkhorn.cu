@@ -1623,6 +1623,418 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) sk_pipe_kernel(SkArgs a
     }
 }
 
+// ------------------------------------------------------------------ 2-CTA wide rows (fp32)
+// 12288 < n <= 40960 (config 5: n = 40000).  A 2-CTA cluster owns a row group
+// and CTA rank q the column slice q (<= 20480 columns), so the clusters pack all
+// 148 SMs (4-CTA clusters strand 16).  Thread t owns the 16-byte chunks
+// t + NT*c (c < CH) of the slice: the row's exponentials y and the sweep's
+// column accumulators stay in registers, g of the slice in shared memory.  Row
+// slices stream through a ring of S sub-row stages (CC chunks per thread each;
+// cp.async.bulk with full/empty mbarriers).  Per row every warp releases its
+// stages as soon as it has loaded them; after the row's named barrier thread 0
+// refills every released stage, so up to S stages (~1.6 rows) stay in flight
+// through the row's reduction and the cluster exchange.  Per row: one warp
+// butterfly, one named barrier, one DSMEM pair exchange with the peer (st.async
+// + mbarrier complete_tx), rank-order combine -- identical in both CTAs.  No
+// exponentials are written back to shared memory.  Sweeps >= 2 use the previous
+// row LSE as the shift (plain sums; out-of-window rows redo the sweep with the
+// max shift), exactly as sk_pipe_kernel.
+template <int NT, int CL> struct W2Sm {
+    uint64_t full[16], empty[16], xbar[4];
+    float xp[4][CL][2];            // [slot][rank][max, sum] of the exchanged CTA pairs
+    float wp[2][NT / 32][2];       // per-warp (max, sum), parity double buffer
+};
+
+__device__ __forceinline__ void named_bar(int id, int nt) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
+}
+
+struct W2Ring {
+    char *base;
+    int S, CPR, nrows;
+    int chunk_floats;      // columns per stage (NT * CC * 4)
+    int width;             // slice width in columns (c1 - c0)
+    unsigned limit;        // chunks to issue in total (single pass) or ~0u
+    unsigned issued;       // thread 0
+    unsigned used;         // every thread (uniform)
+    int cs;                // consumer stage index
+    uint32_t cph;          // consumer phase parity
+    // producer cursor (thread 0): next stage / its empty-barrier parity, the
+    // chunk's part and row, and the row's source pointer -- advanced
+    // incrementally (no divisions on the issue path)
+    int ps, ppart, plr;
+    uint32_t pph;
+    const float *prow;
+    int64_t row_step;      // ngrp * ld
+    const float *row0;     // first row of this group, column c0
+};
+
+__device__ __forceinline__ bool mbar_test_cta(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// Thread 0: refill released stages, up to S chunks ahead of `used` (the chunks
+// this thread has consumed).  block = false only tests the empty barriers (a
+// stage some warp still reads is left for a later call).
+template <int NT, int CL>
+__device__ __forceinline__ void w2_issue(W2Ring &rg, W2Sm<NT, CL> &ws, unsigned used, bool block) {
+    while (rg.issued < used + (unsigned)rg.S && rg.issued < rg.limit) {
+        const int s = rg.ps;
+        if (rg.issued >= (unsigned)rg.S) {
+            if (block) mbar_wait_cta(&ws.empty[s], rg.pph);
+            else if (!mbar_test_cta(&ws.empty[s], rg.pph)) return;
+        }
+        const int col0 = rg.ppart * rg.chunk_floats;
+        const int cols = min(rg.chunk_floats, rg.width - col0);
+        const uint32_t bytes = (uint32_t)(((cols + 3) / 4) * 16);
+        xbar_arm(&ws.full[s], bytes);
+        bulk_g2s(rg.base + (size_t)s * (size_t)rg.chunk_floats * 4, rg.prow + col0, bytes, &ws.full[s]);
+        ++rg.issued;
+        if (++rg.ps == rg.S) { rg.ps = 0; if (rg.issued > (unsigned)rg.S) rg.pph ^= 1u; }
+        if (rg.issued == (unsigned)rg.S) rg.pph = 0;  // the first refill waits on phase 0
+        if (++rg.ppart == rg.CPR) {
+            rg.ppart = 0;
+            if (++rg.plr == rg.nrows) { rg.plr = 0; rg.prow = rg.row0; }
+            else rg.prow += rg.row_step;
+        }
+    }
+}
+
+template <int NT, int CL, int CH, int CC, bool MAXP>
+__device__ __forceinline__ void pass_body_wide(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
+                                               const Slice &sl, W2Sm<NT, CL> &ws, W2Ring &rg, float4 *s_g,
+                                               float *s_shift, unsigned &xi, unsigned *redo) {
+    using T = float;
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool pre = (k == 0);
+    const bool rowonly = (k == max_sweeps + 1);
+    const double *gin = gslot(a, k + 1);
+    const double *fprev = fslot(a, k + 1);
+    double *fout = fslot(a, k);
+    const double ks = SkMath<T>::kScale;
+    const T coef = (T)(coef_d * ks);
+    const T gmax = (T)gmax_d;
+    const int c0 = sl.c0, c1 = sl.c1;
+    const bool writer = (sl.rank == 0) && tid == 0;
+    // g of this thread's chunks (scaled; -inf masks columns past the slice)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        float gv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int col = c0 + (tid + NT * c) * 4 + e;
+            gv[e] = col < c1 ? ((!pre) ? (T)(__ldcg(gin + col) * ks) : T(0)) : neg_inf<T>();
+        }
+        s_g[tid + NT * c] = make_float4(gv[0], gv[1], gv[2], gv[3]);  // read back by this thread only
+    }
+    if constexpr (!MAXP) {
+        for (int i = tid; i < rg.nrows; i += NT) s_shift[i] = (float)(-__ldcg(fprev + sl.grp + i * sl.ngrp) * ks);
+        named_bar(1, NT);
+    }
+    T acc[CH][4];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[c][e] = T(0);
+    double devmax = 0.0;
+    bool bad = false;
+    for (int lr = 0; lr < rg.nrows; ++lr) {
+        // ---- this row's slice: CPR stages of CC chunks per thread
+        T y[CH][4];
+#pragma unroll
+        for (int p = 0; p < CH / CC; ++p) {
+            mbar_wait_cta(&ws.full[rg.cs], rg.cph);
+            const float4 *st = reinterpret_cast<const float4 *>(rg.base + (size_t)rg.cs * rg.chunk_floats * 4);
+#pragma unroll
+            for (int q = 0; q < CC; ++q) {
+                const float4 xv = st[tid + NT * q];
+                y[p * CC + q][0] = xv.x; y[p * CC + q][1] = xv.y; y[p * CC + q][2] = xv.z; y[p * CC + q][3] = xv.w;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ws.empty[rg.cs]);
+            if (++rg.cs == rg.S) { rg.cs = 0; rg.cph ^= 1u; }
+            // refill whatever every warp has released so far (non-blocking)
+            if (tid == 0) w2_issue<NT, CL>(rg, ws, rg.used + (unsigned)(p + 1), false);
+        }
+        rg.used += (unsigned)(CH / CC);
+        // ---- E_ij + g_j (sinkhorn.py:125), shift, exponentials, warp pair
+        T m;
+        if constexpr (MAXP) {
+            m = neg_inf<T>();
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const float4 g4 = s_g[tid + NT * c];
+                const T gl[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const T arg = coef * (gmax - y[c][e]) + gl[e];
+                    y[c][e] = arg;
+                    m = vmax(m, arg);
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) m = vmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+        } else {
+            m = s_shift[lr];  // the row's shift, identical in every warp and both ranks
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const float4 g4 = s_g[tid + NT * c];
+                const T gl[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) y[c][e] = coef * (gmax - y[c][e]) + gl[e];
+            }
+        }
+        const T mx = (m == neg_inf<T>()) ? T(0) : m;
+        T sp[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const T v = SkMath<T>::ex(y[c][e] - mx);
+                y[c][e] = v;
+                sp[e] += v;
+            }
+        T sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        const int par = (int)(xi & 1u);
+        if (lane == 0) { ws.wp[par][warp][0] = m; ws.wp[par][warp][1] = sum; }
+        named_bar(1, NT);
+        // ---- CTA pair: every warp combines the NW warp pairs (fixed xor tree)
+        T M, Sm;
+        {
+            const T mv = lane < NW ? ws.wp[par][lane][0] : neg_inf<T>();
+            const T sv = lane < NW ? ws.wp[par][lane][1] : T(0);
+            if constexpr (MAXP) {
+                M = mv;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) M = vmax(M, __shfl_xor_sync(0xffffffffu, M, off));
+                Sm = (mv != neg_inf<T>()) ? sv * SkMath<T>::ex(mv - M) : T(0);
+            } else {
+                M = m;
+                Sm = sv;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) Sm += __shfl_xor_sync(0xffffffffu, Sm, off);
+        }
+        // ---- exchange with the CL-1 peer CTAs, combine in rank order
+        const int xs = (int)(xi & 3u);
+        const uint32_t xph = (xi >> 2) & 1u;
+        if (tid == 0) xbar_arm(&ws.xbar[xs], (uint32_t)((CL - 1) * 2 * sizeof(T)));
+        if (warp == 0 && lane < CL && lane != sl.rank)
+            st_async_pair(dsmem_map(&ws.xp[xs][sl.rank][0], (uint32_t)lane), M, Sm,
+                          dsmem_map(&ws.xbar[xs], (uint32_t)lane));
+        // every warp passed the row barrier: all of this row's stages are free
+        if (tid == 0) w2_issue<NT, CL>(rg, ws, rg.used, true);
+        xbar_wait(&ws.xbar[xs], xph);
+        T mq[CL], sq[CL];
+#pragma unroll
+        for (int q = 0; q < CL; ++q) {
+            mq[q] = (q == sl.rank) ? M : ws.xp[xs][q][0];
+            sq[q] = (q == sl.rank) ? Sm : ws.xp[xs][q][1];
+        }
+        T Mt, St = T(0);
+        if constexpr (MAXP) {
+            Mt = neg_inf<T>();
+#pragma unroll
+            for (int q = 0; q < CL; ++q) Mt = vmax(Mt, mq[q]);
+#pragma unroll
+            for (int q = 0; q < CL; ++q)
+                if (mq[q] != neg_inf<T>()) St += sq[q] * SkMath<T>::ex(mq[q] - Mt);
+        } else {
+            Mt = mq[0];  // the common shift
+#pragma unroll
+            for (int q = 0; q < CL; ++q) St += sq[q];
+            bad |= !(St >= kShiftLo && St <= kShiftHi) || a.resident == 3;
+        }
+        ++xi;
+        const double lse = (double)Mt + SkMath<T>::lgt(St);  // scaled units
+        if (writer) {
+            const double fnew = -lse * (1.0 / ks);
+            if (pre) devmax = fmax(devmax, SkMath<T>::dev(-fnew));
+            else __stcg(fout + sl.grp + lr * sl.ngrp, fnew);
+        }
+        if (!rowonly && m != neg_inf<T>()) {
+            // column contribution exp(E + g + f_k) = y * 2^(m - lse); the pre-check sums K
+            const T sc = SkMath<T>::ex((T)((double)m + (pre ? 0.0 : -lse)));
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[c][e] += y[c][e] * sc;
+        }
+    }
+    if (!rowonly) {
+        T *cp = static_cast<T *>(a.colpart) + (int64_t)sl.grp * a.ldp;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int col = c0 + (tid + NT * c) * 4;
+            if (col < c1) __stcg(reinterpret_cast<float4 *>(cp + col), make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]));
+        }
+    }
+    if constexpr (!MAXP) {
+        if (bad && tid == 0) atomicOr(redo, 1u);  // `bad` is uniform across the CTA
+    }
+    // dev_{k-1} = max over this group's rows of |expm1(f_{k-1} - f_k)| = |u K v - 1|
+    __shared__ double s_dev[NW];
+    __syncthreads();  // the writer's f_k stores precede the reads below
+    if (sl.rank == 0 && k >= 2) {
+        for (int i = tid; i < rg.nrows; i += NT) {
+            const int row = sl.grp + i * sl.ngrp;
+            devmax = fmax(devmax, SkMath<T>::dev(__ldcg(fprev + row) - __ldcg(fout + row)));
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) devmax = fmax(devmax, __shfl_xor_sync(0xffffffffu, devmax, off));
+    if (lane == 0) s_dev[warp] = devmax;
+    __syncthreads();
+    if (tid == 0) {
+        double d = 0.0;
+        for (int w = 0; w < NW; ++w) d = fmax(d, s_dev[w]);
+        __stcg(a.devpart + blockIdx.x, d);
+        if (a.dslot) atomicMax(a.dslot + (k & 1), (unsigned long long)__double_as_longlong(d));
+    }
+}
+
+template <int NT, int CL, int CH, int CC>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) sk_wide_kernel(SkArgs a, unsigned *bar) {
+    __shared__ int s_k, s_done;
+    if (threadIdx.x == 0) { s_k = a.st->k; s_done = a.st->done | a.st->pending; }
+    __syncthreads();
+    if (a.single_pass && s_done) return;
+    const int k0 = s_k;
+    const int K = a.st->max_sweeps;
+    const double tol = a.st->tol, coef = a.st->coef, gmax = a.st->gmax;
+    const int blk = blockIdx.x, nblk = gridDim.x;
+    uint32_t rank, cid, ncl;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+    asm("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
+    Slice sl{0, a.n, (int)cid, (int)ncl, (int)rank};
+    sl.c0 = min(a.n, (int)rank * a.slice_w);
+    sl.c1 = min(a.n, sl.c0 + a.slice_w);
+    __shared__ W2Sm<NT, CL> ws;
+    extern __shared__ __align__(128) char sk_ring[];
+    W2Ring rg;
+    rg.S = a.stages;
+    rg.CPR = CH / CC;
+    rg.chunk_floats = NT * CC * 4;
+    rg.base = sk_ring;
+    float4 *s_g = reinterpret_cast<float4 *>(sk_ring + (size_t)rg.S * rg.chunk_floats * 4);
+    float *s_shift = reinterpret_cast<float *>(s_g + NT * CH);
+    rg.nrows = max(0, (rows_of(a) - sl.grp + sl.ngrp - 1) / sl.ngrp);
+    rg.width = sl.c1 - sl.c0;
+    rg.limit = a.single_pass ? (unsigned)(rg.nrows * rg.CPR) : ~0u;
+    rg.issued = 0; rg.used = 0; rg.cs = 0; rg.cph = 0;
+    // the tail of a short last chunk is never written by the bulk copies: zero the
+    // ring once so masked columns always read finite values
+    for (int i = threadIdx.x; i < rg.S * NT * CC; i += NT)
+        reinterpret_cast<float4 *>(sk_ring)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < rg.S; ++q) { mbar_init(&ws.full[q], 1); mbar_init(&ws.empty[q], NT / 32); }
+        for (int q = 0; q < 4; ++q) mbar_init(&ws.xbar[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster_sync();  // every peer's barriers exist before the first st.async
+    rg.ps = 0; rg.ppart = 0; rg.plr = 0; rg.pph = 0;
+    rg.row0 = static_cast<const float *>(a.G) + (int64_t)sl.grp * a.ld + sl.c0;
+    rg.prow = rg.row0;
+    rg.row_step = (int64_t)sl.ngrp * a.ld;
+    if (threadIdx.x == 0 && rg.nrows > 0) w2_issue<NT, CL>(rg, ws, 0u, true);
+    unsigned epoch = 0, xi = 0;
+    auto drain = [&]() {  // no bulk copy may be in flight when the CTA exits
+        if (threadIdx.x == 0) {
+            unsigned u = rg.used;
+            int s = rg.cs;
+            uint32_t ph = rg.cph;
+            for (; u < rg.issued; ++u) {
+                mbar_wait_cta(&ws.full[s], ph);
+                if (++s == rg.S) { s = 0; ph ^= 1u; }
+            }
+        }
+        cluster_sync();
+    };
+    unsigned *redo = bar + 64;
+    const bool shift_ok = !a.single_pass && env_shift_ok(a);
+    for (int k = k0;; ++k) {
+        bool maxp = !shift_ok || k <= 1;
+        for (;;) {
+            if (rg.nrows > 0) {
+                if (maxp) pass_body_wide<NT, CL, CH, CC, true>(a, k, K, coef, gmax, sl, ws, rg, s_g, s_shift, xi, redo + (k & 1));
+                else pass_body_wide<NT, CL, CH, CC, false>(a, k, K, coef, gmax, sl, ws, rg, s_g, s_shift, xi, redo + (k & 1));
+            } else if (threadIdx.x == 0) {
+                __stcg(a.devpart + blockIdx.x, 0.0);
+            }
+            if (a.single_pass) { drain(); return; }
+            grid_barrier(bar, nblk, epoch);
+            if (maxp || !__ldcg(redo + (k & 1))) break;
+            // a row left the shift window: recompute the sweep with the max shift
+            if (blk == 0 && threadIdx.x == 0) { a.dslot[k & 1] = 0ull; a.st->redone += 1; }
+            grid_barrier(bar, nblk, epoch);
+            maxp = true;
+        }
+        const double drow = __longlong_as_double((long long)__ldcg(a.dslot + (k & 1)));
+        if (blk == 0 && threadIdx.x == 0) {
+            a.dslot[(k + 1) & 1] = 0ull;  // next sweep's slots
+            redo[(k + 1) & 1] = 0u;
+        }
+        int stop = 0, sweeps = 0, conv = 0, slot = 0;
+        if (k >= 2) {
+            if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
+            else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
+        }
+        if (!stop) {
+            merge_body<float, NT>(a, k, coef, gmax, blk, nblk);
+            grid_barrier(bar, nblk, epoch);
+            if (k == 0) {
+                const double d0 = fmax(drow, __longlong_as_double((long long)__ldcg(a.dslot + 2)));
+                if (d0 < tol) { stop = 1; sweeps = 0; conv = 1; slot = 0; }
+                if (blk == 0 && threadIdx.x == 0) a.st->last_dev = d0;
+                if (stop && blk == 0 && threadIdx.x == 0) a.st->dev = d0;
+            }
+        } else if (blk == 0 && threadIdx.x == 0) {
+            a.st->dev = drow;
+        }
+        if (stop) {
+            if (blk == 0 && threadIdx.x == 0) {
+                a.st->done = 1; a.st->sweeps = sweeps; a.st->converged = conv; a.st->slot = slot;
+                a.st->k = k + 1;
+            }
+            drain();
+            return;
+        }
+    }
+}
+
+template <int NT, int CL, int CH> void *wide2_fn() { return (void *)sk_wide_kernel<NT, CL, CH, 2>; }
+void *wide2_for(int nt, int cl, int ch) {
+#define GOAT_W2(NT_, CL_)                                \
+    if (nt == NT_ && cl == CL_) {                        \
+        switch (ch) {                                    \
+            case 4: return wide2_fn<NT_, CL_, 4>();      \
+            case 6: return wide2_fn<NT_, CL_, 6>();      \
+            case 8: return wide2_fn<NT_, CL_, 8>();      \
+            case 10: return wide2_fn<NT_, CL_, 10>();    \
+        }                                                \
+    }
+    GOAT_W2(512, 2)
+    GOAT_W2(256, 4)
+#undef GOAT_W2
+    throw Error(GOAT_ENOTSUP, "sinkhorn: no wide-row kernel for threads=" + std::to_string(nt) + " cluster=" +
+                                  std::to_string(cl) + " chunks=" + std::to_string(ch));
+}
+
 // ------------------------------------------------------------------ row-sharded sweep
 // Column sums of this block's pass (fixed CTA order, fp64) and its max row deviation.
 template <class T>
@@ -2134,7 +2546,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
         __syncthreads();
         sk_stamp(a, k, 4);
         if (!rowonly) {
-            T *cp = static_cast<T *>(a.colpart) + (int64_t)grp * a.ldp;
+            // double-buffered by sweep parity: a CTA of another cluster may still be
+            // merging this group's sweep-(k-1) partials (there is one grid barrier per
+            // sweep); the k-2 buffer is free since every CTA passed barrier k-1 after
+            // its merge of sweep k-2.
+            T *cp = static_cast<T *>(a.colpart) + ((int64_t)(k & 1) * ngrp + grp) * a.ldp;
             for (int c = tid; c < SW; c += kTileThreads) {
                 if (c0 + c >= c1) continue;
                 T v = T(0);
@@ -2170,7 +2586,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
         // ---- merge of this CTA's columns (fixed order over the row groups, fp64).
         // (Measured: this plain loop beats batching all partial loads or splitting a
         // column's groups over two threads -- profiles/round1_sk_tile.md.)
-        const T *cpa = static_cast<const T *>(a.colpart);
+        const T *cpa = static_cast<const T *>(a.colpart) + (int64_t)(k & 1) * ngrp * a.ldp;
         const double tiny = sizeof(T) == 4 ? 1e-30 : 1e-290;
         double dloc = 0.0;
         for (int c = tid; c < SW; c += kTileThreads) {
@@ -2404,7 +2820,8 @@ template <class T> bool tile_plan_width(int n, int num_sms, SkPlan &p, int cl, i
     p.ngrp = (n + rows_g - 1) / rows_g;
     p.nblk = p.ngrp * cl;
     p.merge_blocks = 1;
-    p.colpart_bytes = (size_t)std::max(p.ngrp, num_sms * 2) * round_up(n, 8) * sizeof(T);
+    // two parity buffers of ngrp rows (sk_tile_kernel double-buffers the partials)
+    p.colpart_bytes = (size_t)std::max(2 * p.ngrp, num_sms * 2) * round_up(n, 8) * sizeof(T);
     return true;
 }
 
@@ -2427,6 +2844,59 @@ template <class T> bool tile_plan(int n, int num_sms, SkPlan &p) {
     return tile_plan_width<T>(n, num_sms, p, cl, cpl);
 }
 
+// Wide fp32 rows, 12288 < n <= 40960 (sk_wide_kernel): a cluster splits each
+// row into CL slices of <= 10 chunks per thread held in registers; g of the
+// slice and an S-stage ring of sub-row stages in shared memory.  Shapes: one
+// 512-thread CTA per SM in 2-CTA clusters, or two 256-thread CTAs per SM in
+// 4-CTA clusters (GOAT_SK_WIDE_CL=2|4).
+bool wide2_plan(int n, int mrows, int num_sms, SkPlan &p) {
+    const int mode = env_int("GOAT_SK_WIDE", 1);
+    if (mode == 0) return false;
+    if (mode != 2 && (n <= 12288 || n > 40960)) return false;
+    constexpr int VW = 4, CC = 2;
+    const int CL = env_int("GOAT_SK_WIDE_CL", 2) == 4 ? 4 : 2;
+    const int NT = CL == 2 ? 512 : 256;
+    const int per_sm = CL == 2 ? 1 : 2;
+    const int sw = (int)round_up(ceil_div(n, CL), 8 * VW);
+    int ch = ceil_div(ceil_div(sw, VW), NT);
+    ch = (int)round_up(std::max(ch, 4), CC);
+    if (ch > 10) return false;
+    p = SkPlan{};
+    p.nt = NT; p.cl = CL; p.ch = ch; p.rows = 1; p.slice_w = sw; p.wide2 = true; p.persistent = true;
+    p.stage_bytes = NT * CC * 16;
+    void *const kfn = wide2_for(NT, CL, ch);
+    // the ring takes what g and the shift table leave of this CTA's share of shared memory
+    const size_t gl = (size_t)NT * ch * 16, budget = (228 * 1024) / per_sm - 3 * 1024;
+    const int rows_max = ceil_div(mrows, std::max(1, per_sm * num_sms / CL));
+    const size_t shift = round_up((size_t)(rows_max + 64) * 4, 128);
+    if (gl + shift >= budget) return false;
+    int S = (int)((budget - gl - shift) / p.stage_bytes);
+    S = std::min(16, S);
+    if (const int st = env_int("GOAT_SK_STAGES", 0)) S = std::min(S, std::max(3, st));
+    if (S < 2 * (ch / CC) && S < 6) return false;
+    p.stages = S;
+    p.smem = (size_t)S * p.stage_bytes + gl + shift;
+    GOAT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    cudaLaunchAttribute attrs[2];
+    SkPlan q = p;
+    q.nblk = CL * num_sms;
+    cudaLaunchConfig_t cfg = persistent_config(q, nullptr, attrs);
+    cudaLaunchAttribute cattr = attrs[1];
+    cfg.attrs = &cattr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    GOAT_CUDA(cudaOccupancyMaxActiveClusters(&ncl, kfn, &cfg));
+    if (ncl < 1) return false;
+    int ngrp = std::max(1, std::min(mrows, ncl));
+    if (const int force = env_int("GOAT_SK_BLOCKS", 0)) ngrp = std::max(1, std::min({force / CL, mrows, ncl}));
+    if (ceil_div(mrows, ngrp) + 64 > (int)(shift / 4)) return false;
+    p.ngrp = ngrp;
+    p.nblk = CL * ngrp;
+    p.merge_blocks = std::max(1, std::min((n + 7) / 8, 4 * num_sms));
+    p.colpart_bytes = (size_t)std::max(p.nblk, num_sms * 2) * round_up(n, 8) * sizeof(float);
+    return true;
+}
+
 template <class T> SkPlan sk_plan(int n, int num_sms, int mrows, bool sharded) {
     if (mrows < 0) mrows = n;
     constexpr int VW = VecT<T>::W;
@@ -2438,6 +2908,10 @@ template <class T> SkPlan sk_plan(int n, int num_sms, int mrows, bool sharded) {
     // fp32 rows of more than 6144 columns take the bulk-copy pipeline (measured at
     // n = 8192: 0.084 vs 0.104 ms; at n = 5000 the register kernel wins, 0.043 vs
     // 0.050); GOAT_SK_PIPE=3 forces it for any n, 0 disables it
+    if (sizeof(T) == 4) {
+        SkPlan wp;  // committed only if complete
+        if (wide2_plan(n, mrows, num_sms, wp)) return wp;
+    }
     SkPlan pp;  // a pipe plan is committed only if it is complete
     // (and 4096 < n <= 6144 with 2-row bands: n = 5000 0.0395 vs 0.0425 ms)
     if (sizeof(T) == 4 && (ceil_div(ceil_div(n, VW), kThreads) > 6 || (n > 4096 && n <= 6144) ||
@@ -2583,8 +3057,10 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
     cudaLaunchAttribute attrs[2];
     cudaLaunchConfig_t cfg = persistent_config(p, s, attrs);
     if (p.tile && args.single_pass) throw Error(GOAT_ENOTSUP, "sinkhorn: the tile plan has no single-pass mode");
-    void *fn = p.tile ? tile_for<T>(p.cl, p.ch, p.rows)
-                      : p.pipe ? pipe_for(p.ch, p.cl, p.nt, p.rows) : persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
+    void *fn = p.tile    ? tile_for<T>(p.cl, p.ch, p.rows)
+               : p.wide2 ? wide2_for(p.nt, p.cl, p.ch)
+               : p.pipe  ? pipe_for(p.ch, p.cl, p.nt, p.rows)
+                         : persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
     int rows_g = p.tile_rows;
     void *tparams[] = {&args, &bar, &rows_g};
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, p.tile ? tparams : params);

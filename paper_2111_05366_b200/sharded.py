@@ -309,29 +309,42 @@ def _csr_rows_to_device(M, dev, dtype):
     return (rowptr, col, torch.from_numpy(np.ascontiguousarray(M.data)).to(dev, dtype))
 
 
+def prepare_csr(A, B, *, precision="fp32", group=None, gemm="auto"):
+    """Upload this rank's CSR rows of A and A^T and the whole CSR of B (and B^T)
+    and set up the shard handle; returns (backend, comm) for ``sharded_fw_core``
+    with ``A_rows=None`` (inputs resident on the device)."""
+    from . import engine
+    comm = Comm(group)
+    A = engine.as_csr(A, "A")
+    B = engine.as_csr(B, "B")
+    layout = ShardLayout(A.shape[0], comm.world, comm.rank)
+    be = GpuShardBackend(layout, precision, gemm=gemm)
+    r0, m = layout.r0, layout.m
+    sym = (A != A.T).nnz == 0 and (B != B.T).nnz == 0
+    dev, dt = be.dev, be.dtype
+    a_rows = _csr_rows_to_device(A[r0:r0 + m], dev, dt)
+    At = A.T.tocsr(); At.sort_indices()
+    at_rows = None if sym else _csr_rows_to_device(At[r0:r0 + m], dev, dt)
+    b_full = _csr_rows_to_device(B, dev, dt)
+    Bt = B.T.tocsr(); Bt.sort_indices()
+    bt_full = None if sym else _csr_rows_to_device(Bt, dev, dt)
+    be.setup_csr(a_rows, at_rows, b_full, bt_full)
+    return be, comm
+
+
 def sharded_match(A, B, *, precision="fp32", group=None, gemm="auto", **kw) -> ShardedResult:
     """Row-sharded GOAT on this rank's GPU (every rank passes the full matrices;
     each uploads only its own rows of A and A^T, and B).  Dense host arrays run the
     GEMM gradient; scipy.sparse / CSR graphs run the SpMM gradient on CSR rows."""
     from . import engine
+    if engine.is_sparse(A) or engine.is_sparse(B):
+        be, comm = prepare_csr(A, B, precision=precision, group=group, gemm=gemm)
+        return sharded_fw_core(be, comm, None, None, None, **kw)
     comm = Comm(group)
-    n = A.shape[0] if not isinstance(A, engine.CsrGraphType()) else A.n
+    n = A.shape[0]
     layout = ShardLayout(n, comm.world, comm.rank)
     be = GpuShardBackend(layout, precision, gemm=gemm)
     r0, m = layout.r0, layout.m
-    if engine.is_sparse(A) or engine.is_sparse(B):
-        A = engine.as_csr(A, "A")
-        B = engine.as_csr(B, "B")
-        sym = (A != A.T).nnz == 0 and (B != B.T).nnz == 0
-        dev, dt = be.dev, be.dtype
-        a_rows = _csr_rows_to_device(A[r0:r0 + m], dev, dt)
-        At = A.T.tocsr(); At.sort_indices()
-        at_rows = None if sym else _csr_rows_to_device(At[r0:r0 + m], dev, dt)
-        b_full = _csr_rows_to_device(B, dev, dt)
-        Bt = B.T.tocsr(); Bt.sort_indices()
-        bt_full = None if sym else _csr_rows_to_device(Bt, dev, dt)
-        be.setup_csr(a_rows, at_rows, b_full, bt_full)
-        return sharded_fw_core(be, comm, None, None, None, **kw)
     sym = bool(np.array_equal(A, A.T) and np.array_equal(B, B.T))
     A_rows = be.upload(A[r0:r0 + m], layout.m_pad)
     AT_rows = None if sym else be.upload(np.ascontiguousarray(A.T[r0:r0 + m]), layout.m_pad)
