@@ -1364,6 +1364,7 @@ int goat_bench_sweep(goat_handle *h, int64_t n, const void *dG, int64_t ld, int3
                 GOAT_CUDA(cudaMemcpy(t.data(), tb.p, t.size() * 8, cudaMemcpyDeviceToHost));
                 unsigned long long t0 = ~0ull;
                 for (int b = 0; b < nb; ++b) if (t[b * 16]) t0 = std::min(t0, t[b * 16]);
+                if (getenv("GOAT_SK_TRACE_RAW")) t0 = 0;  // accumulated phase cycles, not stamps
                 fprintf(stderr, "sk_trace n=%d nblk=%d cl=%d stages=%d (ns after first pass start): stamp min/median/max\n", (int)n, nb, plan.cl, plan.stages);
                 for (int i = 0; i < 16; ++i) {
                     std::vector<double> v;

@@ -30,6 +30,7 @@ struct SkArgs {
     unsigned long long *trace = nullptr;  // diagnostics: per-CTA phase timestamps of sweep trace_k
     int trace_k = -1;
     int stage_bytes = 0;
+    int dbg = 0;        // timing experiments only (GOAT_SK_DBG): drop parts of the wide-row pass
 };
 
 struct SkPlan {
@@ -49,6 +50,7 @@ struct SkPlan {
     bool pipe = false;        // wide fp32 rows: decoupled bulk-copy pipeline (sk_pipe_kernel)
     bool tile = false;        // small n: shared-memory-resident tiles, one barrier per sweep (sk_tile_kernel)
     bool wide2 = false;       // 12288 < n <= 40960 fp32: 2-CTA clusters, registers hold y and the column sums (sk_wide_kernel)
+    bool wide_tm = false;     // wide2 with rows parked in TMEM for a lagged finish (sk_wide_kernel<..., TM>)
     int tile_rows = 0;        // rows per row group of the tile kernel
 };
 

@@ -1649,24 +1649,28 @@ __device__ __forceinline__ void named_bar(int id, int nt) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
 }
 
+// Producer cursor (thread 0 only; kept in shared memory so it costs the compute
+// threads no registers): chunks issued / to issue, next stage and its empty-barrier
+// parity, the chunk's part and row, the row's source pointer -- advanced
+// incrementally (no divisions on the issue path).
+struct W2Prod {
+    unsigned limit, issued;
+    int ps, ppart, plr, width, hint;
+    uint32_t pph;
+    const float *prow, *row0;
+    int64_t row_step;      // ngrp * ld
+    uint64_t pol;          // L2 evict_first policy (G streams through once per sweep)
+};
+
 struct W2Ring {
     char *base;
     int S, CPR, nrows;
     int chunk_floats;      // columns per stage (NT * CC * 4)
-    int width;             // slice width in columns (c1 - c0)
-    unsigned limit;        // chunks to issue in total (single pass) or ~0u
-    unsigned issued;       // thread 0
-    unsigned used;         // every thread (uniform)
+    unsigned used;         // chunks consumed (every thread, uniform)
     int cs;                // consumer stage index
     uint32_t cph;          // consumer phase parity
-    // producer cursor (thread 0): next stage / its empty-barrier parity, the
-    // chunk's part and row, and the row's source pointer -- advanced
-    // incrementally (no divisions on the issue path)
-    int ps, ppart, plr;
-    uint32_t pph;
-    const float *prow;
-    int64_t row_step;      // ngrp * ld
-    const float *row0;     // first row of this group, column c0
+    int nb;                // thread 0 also refills without blocking right after its row loads
+    W2Prod *pr;
 };
 
 __device__ __forceinline__ bool mbar_test_cta(uint64_t *bar, uint32_t parity) {
@@ -1688,26 +1692,67 @@ __device__ __forceinline__ bool mbar_test_cta(uint64_t *bar, uint32_t parity) {
 // stage some warp still reads is left for a later call).
 template <int NT, int CL>
 __device__ __forceinline__ void w2_issue(W2Ring &rg, W2Sm<NT, CL> &ws, unsigned used, bool block) {
-    while (rg.issued < used + (unsigned)rg.S && rg.issued < rg.limit) {
-        const int s = rg.ps;
-        if (rg.issued >= (unsigned)rg.S) {
-            if (block) mbar_wait_cta(&ws.empty[s], rg.pph);
-            else if (!mbar_test_cta(&ws.empty[s], rg.pph)) return;
+    W2Prod &pr = *rg.pr;
+    while (pr.issued < used + (unsigned)rg.S && pr.issued < pr.limit) {
+        const int s = pr.ps;
+        if (pr.issued >= (unsigned)rg.S) {
+            if (block) mbar_wait_cta(&ws.empty[s], pr.pph);
+            else if (!mbar_test_cta(&ws.empty[s], pr.pph)) return;
         }
-        const int col0 = rg.ppart * rg.chunk_floats;
-        const int cols = min(rg.chunk_floats, rg.width - col0);
+        const int col0 = pr.ppart * rg.chunk_floats;
+        const int cols = min(rg.chunk_floats, pr.width - col0);
         const uint32_t bytes = (uint32_t)(((cols + 3) / 4) * 16);
+        char *dst = rg.base + (size_t)s * (size_t)rg.chunk_floats * 4;
         xbar_arm(&ws.full[s], bytes);
-        bulk_g2s(rg.base + (size_t)s * (size_t)rg.chunk_floats * 4, rg.prow + col0, bytes, &ws.full[s]);
-        ++rg.issued;
-        if (++rg.ps == rg.S) { rg.ps = 0; if (rg.issued > (unsigned)rg.S) rg.pph ^= 1u; }
-        if (rg.issued == (unsigned)rg.S) rg.pph = 0;  // the first refill waits on phase 0
-        if (++rg.ppart == rg.CPR) {
-            rg.ppart = 0;
-            if (++rg.plr == rg.nrows) { rg.plr = 0; rg.prow = rg.row0; }
-            else rg.prow += rg.row_step;
+        if (pr.hint) bulk_g2s_hint(dst, pr.prow + col0, bytes, &ws.full[s], pr.pol);
+        else bulk_g2s(dst, pr.prow + col0, bytes, &ws.full[s]);
+        ++pr.issued;
+        if (++pr.ps == rg.S) { pr.ps = 0; if (pr.issued > (unsigned)rg.S) pr.pph ^= 1u; }
+        if (pr.issued == (unsigned)rg.S) pr.pph = 0;  // the first refill waits on phase 0
+        if (++pr.ppart == rg.CPR) {
+            pr.ppart = 0;
+            if (++pr.plr == rg.nrows) { pr.plr = 0; pr.prow = pr.row0; }
+            else pr.prow += pr.row_step;
         }
     }
+}
+
+// One row slice into registers: wait for all of the row's stages first, issue
+// every shared-memory load, then release the stages together (the loads overlap;
+// a per-stage wait/load/release chain serialised the warp that also refills).
+template <int NT, int CL, int CH, int CC>
+__device__ __forceinline__ void w2_load_row(W2Ring &rg, W2Sm<NT, CL> &ws, float (&y)[CH][4], int tid, int lane) {
+    constexpr int CPR = CH / CC;
+    int sidx[CPR];
+    {
+        int cs = rg.cs;
+        uint32_t ph = rg.cph;
+#pragma unroll
+        for (int p = 0; p < CPR; ++p) {
+            sidx[p] = cs;
+            mbar_wait_cta(&ws.full[cs], ph);
+            if (++cs == rg.S) { cs = 0; ph ^= 1u; }
+        }
+        rg.cs = cs;
+        rg.cph = ph;
+    }
+#pragma unroll
+    for (int p = 0; p < CPR; ++p) {
+        const float4 *st = reinterpret_cast<const float4 *>(rg.base + (size_t)sidx[p] * rg.chunk_floats * 4);
+#pragma unroll
+        for (int q = 0; q < CC; ++q) {
+            const float4 xv = st[tid + NT * q];
+            y[p * CC + q][0] = xv.x; y[p * CC + q][1] = xv.y; y[p * CC + q][2] = xv.z; y[p * CC + q][3] = xv.w;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < CPR; ++p) mbar_arrive(&ws.empty[sidx[p]]);
+    }
+    rg.used += (unsigned)CPR;
+    // refill whatever every warp has released so far (non-blocking)
+    if (tid == 0 && rg.nb) w2_issue<NT, CL>(rg, ws, rg.used, false);
 }
 
 template <int NT, int CL, int CH, int CC, bool MAXP>
@@ -1752,22 +1797,7 @@ __device__ __forceinline__ void pass_body_wide(const SkArgs &a, int k, int max_s
     for (int lr = 0; lr < rg.nrows; ++lr) {
         // ---- this row's slice: CPR stages of CC chunks per thread
         T y[CH][4];
-#pragma unroll
-        for (int p = 0; p < CH / CC; ++p) {
-            mbar_wait_cta(&ws.full[rg.cs], rg.cph);
-            const float4 *st = reinterpret_cast<const float4 *>(rg.base + (size_t)rg.cs * rg.chunk_floats * 4);
-#pragma unroll
-            for (int q = 0; q < CC; ++q) {
-                const float4 xv = st[tid + NT * q];
-                y[p * CC + q][0] = xv.x; y[p * CC + q][1] = xv.y; y[p * CC + q][2] = xv.z; y[p * CC + q][3] = xv.w;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ws.empty[rg.cs]);
-            if (++rg.cs == rg.S) { rg.cs = 0; rg.cph ^= 1u; }
-            // refill whatever every warp has released so far (non-blocking)
-            if (tid == 0) w2_issue<NT, CL>(rg, ws, rg.used + (unsigned)(p + 1), false);
-        }
-        rg.used += (unsigned)(CH / CC);
+        w2_load_row<NT, CL, CH, CC>(rg, ws, y, tid, lane);
         // ---- E_ij + g_j (sinkhorn.py:125), shift, exponentials, warp pair
         T m;
         if constexpr (MAXP) {
@@ -1906,7 +1936,250 @@ __device__ __forceinline__ void pass_body_wide(const SkArgs &a, int k, int max_s
     }
 }
 
-template <int NT, int CL, int CH, int CC>
+// TMEM-lagged variant (TM) of the wide-row pass: as pass_body_wide, but a row's
+// exponentials are parked in tensor memory (tcgen05.st, 32x32b: each thread its
+// own TMEM lane) while the peer's pair of the row travels, and the row is
+// finished one row later (tcgen05.ld back into registers, acc += y * sc) -- the
+// cluster exchange latency hides behind the next row's loads and exponentials.
+// TMEM holds two row slots per warp: (warp>>2)*2 + slot selects CH*4 columns of
+// the warp's lane quadrant (warp & 3).
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const float *v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, float *v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int NT, int CL, int CH, int CC, bool MAXP>
+__device__ __forceinline__ void pass_body_tm(const SkArgs &a, int k, int max_sweeps, double coef_d, double gmax_d,
+                                             const Slice &sl, W2Sm<NT, CL> &ws, W2Ring &rg, float4 *s_g,
+                                             float *s_shift, unsigned &xi, unsigned *redo, uint32_t tbase) {
+    using T = float;
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool pre = (k == 0);
+    const bool rowonly = (k == max_sweeps + 1);
+    const double *gin = gslot(a, k + 1);
+    const double *fprev = fslot(a, k + 1);
+    double *fout = fslot(a, k);
+    const double ks = SkMath<T>::kScale;
+    const T coef = (T)(coef_d * ks);
+    const T gmax = (T)gmax_d;
+    const int c0 = sl.c0, c1 = sl.c1;
+    const bool writer = (sl.rank == 0) && tid == 0;
+    const uint32_t tq = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+    // g of this thread's chunks (scaled; -inf masks columns past the slice) in TMEM
+    // columns [(8 + (warp>>2)) * CH*4, ...) of the warp's lane quadrant
+    const uint32_t tg = tq + (uint32_t)((8 + (warp >> 2)) * CH * 4);
+    {
+        float gv[CH][4];
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int col = c0 + (tid + NT * c) * 4 + e;
+                gv[c][e] = col < c1 ? ((!pre) ? (T)(__ldcg(gin + col) * ks) : T(0)) : neg_inf<T>();
+            }
+#pragma unroll
+        for (int c = 0; c < CH; c += 2) tm_st8(tg + (uint32_t)(c * 4), &gv[c][0]);
+        tm_wait_st();
+    }
+    if constexpr (!MAXP) {
+        for (int i = tid; i < rg.nrows; i += NT) s_shift[i] = (float)(-__ldcg(fprev + sl.grp + i * sl.ngrp) * ks);
+        named_bar(1, NT);
+    }
+    T acc[CH][4];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[c][e] = T(0);
+    double devmax = 0.0;
+    bool bad = false;
+    const unsigned x0 = xi;
+    T mprev = T(0), Mp = T(0), Sp = T(0);
+#ifdef GOAT_SK_PHASE_TRACE
+    // phase-cycle accounting of thread 0 for the traced sweep (GOAT_SK_TRACE=k, GOAT_SK_TRACE_RAW=1;
+    // build with -DGOAT_SK_PHASE_TRACE)
+    const bool tr = a.trace && k == a.trace_k && tid == 0;
+    unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tl = tr ? clock64() : 0;
+    auto tick = [&](int i) { if (tr) { const unsigned long long t = clock64(); tacc[i] += t - tl; tl = t; } };
+#else
+    auto tick = [](int) {};
+#endif
+    for (int it = 0; it <= rg.nrows; ++it) {
+        T m = T(0), Mc = T(0), Sc = T(0);
+        if (it < rg.nrows) {
+            // ---- row it: loads, exponentials, this CTA's pair; exponentials -> TMEM
+            T y[CH][4];
+            tick(7);
+            w2_load_row<NT, CL, CH, CC>(rg, ws, y, tid, lane);
+            tick(1);
+            // E_ij + g_j (sinkhorn.py:125), g streamed back from TMEM two chunks at a time
+#pragma unroll
+            for (int c = 0; c < CH; c += 2) {
+                float gl[2][4];
+                tm_ld8(tg + (uint32_t)(c * 4), &gl[0][0]);
+                tm_wait_ld();
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) y[c + q][e] = coef * (gmax - y[c + q][e]) + gl[q][e];
+            }
+            if constexpr (MAXP) {
+                m = neg_inf<T>();
+#pragma unroll
+                for (int c = 0; c < CH; ++c)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) m = vmax(m, y[c][e]);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) m = vmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+            } else {
+                m = s_shift[it];
+            }
+            const T mx = (m == neg_inf<T>()) ? T(0) : m;
+            T sp[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const T v = SkMath<T>::ex(y[c][e] - mx);
+                    y[c][e] = v;
+                    sp[e] += v;
+                }
+            // park the exponentials until the row is finished (next iteration)
+            if (!rowonly) {
+                const uint32_t tcol = tq + (uint32_t)(((warp >> 2) * 2 + (it & 1)) * CH * 4);
+#pragma unroll
+                for (int c = 0; c < CH; c += 2) tm_st8(tcol + (uint32_t)(c * 4), &y[c][0]);
+            }
+            T sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+            const int par = it & 1;
+            if (lane == 0) { ws.wp[par][warp][0] = m; ws.wp[par][warp][1] = sum; }
+            tick(2);
+            named_bar(1, NT);
+            const T mv = lane < NW ? ws.wp[par][lane][0] : neg_inf<T>();
+            tick(3);
+            const T sv = lane < NW ? ws.wp[par][lane][1] : T(0);
+            if constexpr (MAXP) {
+                Mc = mv;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) Mc = vmax(Mc, __shfl_xor_sync(0xffffffffu, Mc, off));
+                Sc = (mv != neg_inf<T>()) ? sv * SkMath<T>::ex(mv - Mc) : T(0);
+            } else {
+                Mc = m;
+                Sc = sv;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) Sc += __shfl_xor_sync(0xffffffffu, Sc, off);
+            const unsigned xr = x0 + (unsigned)it;
+            if (tid == 0) xbar_arm(&ws.xbar[xr & 3u], (uint32_t)((CL - 1) * 2 * sizeof(T)));
+            if (warp == 0 && lane < CL && lane != sl.rank)
+                st_async_pair(dsmem_map(&ws.xp[xr & 3u][sl.rank][0], (uint32_t)lane), Mc, Sc,
+                              dsmem_map(&ws.xbar[xr & 3u], (uint32_t)lane));
+            // every warp passed the row barrier: all of this row's stages are free
+            if (tid == 0) w2_issue<NT, CL>(rg, ws, rg.used, true);
+            tick(4);
+        }
+        if (it >= 1) {
+            // ---- finish row it-1 from every rank's pair (rank order)
+            const int lr = it - 1;
+            const unsigned xr = x0 + (unsigned)lr;
+            xbar_wait(&ws.xbar[xr & 3u], (xr >> 2) & 1u);
+            tick(5);
+            T mq[CL], sq[CL];
+#pragma unroll
+            for (int q = 0; q < CL; ++q) {
+                mq[q] = (q == sl.rank) ? Mp : ws.xp[xr & 3u][q][0];
+                sq[q] = (q == sl.rank) ? Sp : ws.xp[xr & 3u][q][1];
+            }
+            T Mt, St = T(0);
+            if constexpr (MAXP) {
+                Mt = neg_inf<T>();
+#pragma unroll
+                for (int q = 0; q < CL; ++q) Mt = vmax(Mt, mq[q]);
+#pragma unroll
+                for (int q = 0; q < CL; ++q)
+                    if (mq[q] != neg_inf<T>()) St += sq[q] * SkMath<T>::ex(mq[q] - Mt);
+            } else {
+                Mt = mq[0];  // the common shift
+#pragma unroll
+                for (int q = 0; q < CL; ++q) St += sq[q];
+                bad |= !(St >= kShiftLo && St <= kShiftHi) || a.resident == 3;
+            }
+            const double lse = (double)Mt + SkMath<T>::lgt(St);  // scaled units
+            if (writer) {
+                const double fnew = -lse * (1.0 / ks);
+                if (pre) devmax = fmax(devmax, SkMath<T>::dev(-fnew));
+                else __stcg(fout + sl.grp + lr * sl.ngrp, fnew);
+            }
+            if (!rowonly) {
+                // column contribution exp(E + g + f_k) = y * 2^(m - lse); the pre-check sums K
+                T yl[CH][4];
+                const uint32_t tcol = tq + (uint32_t)(((warp >> 2) * 2 + (lr & 1)) * CH * 4);
+                tm_wait_st();
+#pragma unroll
+                for (int c = 0; c < CH; c += 2) tm_ld8(tcol + (uint32_t)(c * 4), &yl[c][0]);
+                tm_wait_ld();
+                const T sc = (mprev == neg_inf<T>()) ? T(0) : SkMath<T>::ex((T)((double)mprev + (pre ? 0.0 : -lse)));
+#pragma unroll
+                for (int c = 0; c < CH; ++c)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[c][e] += yl[c][e] * sc;
+            }
+            tick(6);
+        }
+        mprev = m;
+        Mp = Mc;
+        Sp = Sc;
+    }
+    xi = x0 + (unsigned)rg.nrows;
+#ifdef GOAT_SK_PHASE_TRACE
+    if (tr) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a.trace[blockIdx.x * 16 + i] = tacc[i] + 1;
+    }
+#endif
+    if (!rowonly) {
+        T *cp = static_cast<T *>(a.colpart) + (int64_t)sl.grp * a.ldp;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int col = c0 + (tid + NT * c) * 4;
+            if (col < c1) __stcg(reinterpret_cast<float4 *>(cp + col), make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]));
+        }
+    }
+    if constexpr (!MAXP) {
+        if (bad && tid == 0) atomicOr(redo, 1u);  // `bad` is uniform across the CTA
+    }
+    __shared__ double s_dev[NW];
+    __syncthreads();  // the writer's f_k stores precede the reads below
+    if (sl.rank == 0 && k >= 2) {
+        for (int i = tid; i < rg.nrows; i += NT) {
+            const int row = sl.grp + i * sl.ngrp;
+            devmax = fmax(devmax, SkMath<T>::dev(__ldcg(fprev + row) - __ldcg(fout + row)));
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) devmax = fmax(devmax, __shfl_xor_sync(0xffffffffu, devmax, off));
+    if (lane == 0) s_dev[warp] = devmax;
+    __syncthreads();
+    if (tid == 0) {
+        double d = 0.0;
+        for (int w = 0; w < NW; ++w) d = fmax(d, s_dev[w]);
+        __stcg(a.devpart + blockIdx.x, d);
+        if (a.dslot) atomicMax(a.dslot + (k & 1), (unsigned long long)__double_as_longlong(d));
+    }
+}
+
+template <int NT, int CL, int CH, int CC, bool TM>
 __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) sk_wide_kernel(SkArgs a, unsigned *bar) {
     __shared__ int s_k, s_done;
     if (threadIdx.x == 0) { s_k = a.st->k; s_done = a.st->done | a.st->pending; }
@@ -1931,11 +2204,26 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) sk_wide_kernel(SkArgs
     rg.chunk_floats = NT * CC * 4;
     rg.base = sk_ring;
     float4 *s_g = reinterpret_cast<float4 *>(sk_ring + (size_t)rg.S * rg.chunk_floats * 4);
-    float *s_shift = reinterpret_cast<float *>(s_g + NT * CH);
+    float *s_shift = reinterpret_cast<float *>(s_g + (TM ? 0 : NT * CH));
     rg.nrows = max(0, (rows_of(a) - sl.grp + sl.ngrp - 1) / sl.ngrp);
-    rg.width = sl.c1 - sl.c0;
-    rg.limit = a.single_pass ? (unsigned)(rg.nrows * rg.CPR) : ~0u;
-    rg.issued = 0; rg.used = 0; rg.cs = 0; rg.cph = 0;
+    __shared__ W2Prod s_prod;
+    rg.pr = &s_prod;
+    rg.used = 0; rg.cs = 0; rg.cph = 0;
+    rg.nb = (a.dbg & 128) ? 0 : 1;
+    if (threadIdx.x == 0) {
+        W2Prod &pr = s_prod;
+        pr.width = sl.c1 - sl.c0;
+        pr.limit = a.single_pass ? (unsigned)(rg.nrows * rg.CPR) : ~0u;
+        pr.issued = 0;
+        pr.ps = 0; pr.ppart = 0; pr.plr = 0; pr.pph = 0;
+        pr.row0 = static_cast<const float *>(a.G) + (int64_t)sl.grp * a.ld + sl.c0;
+        pr.prow = pr.row0;
+        pr.row_step = (int64_t)sl.ngrp * a.ld;
+        // bulk copies stream G through L2 once per sweep: evict_first unless GOAT_SK_DBG bit 64
+        pr.hint = (a.dbg & 64) ? 0 : 1;
+        pr.pol = 0;
+        if (pr.hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pr.pol));
+    }
     // the tail of a short last chunk is never written by the bulk copies: zero the
     // ring once so masked columns always read finite values
     for (int i = threadIdx.x; i < rg.S * NT * CC; i += NT)
@@ -1946,11 +2234,22 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) sk_wide_kernel(SkArgs
         for (int q = 0; q < 4; ++q) mbar_init(&ws.xbar[q], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // TM: 512 TMEM columns (two parked rows per warp: 4 warps x 2 slots x CH*4 columns
+    // per lane quadrant), allocated by warp 0
+    __shared__ uint32_t s_tmem;
+    if constexpr (TM) {
+        if ((threadIdx.x >> 5) == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
     cluster_sync();  // every peer's barriers exist before the first st.async
-    rg.ps = 0; rg.ppart = 0; rg.plr = 0; rg.pph = 0;
-    rg.row0 = static_cast<const float *>(a.G) + (int64_t)sl.grp * a.ld + sl.c0;
-    rg.prow = rg.row0;
-    rg.row_step = (int64_t)sl.ngrp * a.ld;
+    uint32_t tbase = 0;
+    if constexpr (TM) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tbase = s_tmem;
+    }
     if (threadIdx.x == 0 && rg.nrows > 0) w2_issue<NT, CL>(rg, ws, 0u, true);
     unsigned epoch = 0, xi = 0;
     auto drain = [&]() {  // no bulk copy may be in flight when the CTA exits
@@ -1958,12 +2257,19 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) sk_wide_kernel(SkArgs
             unsigned u = rg.used;
             int s = rg.cs;
             uint32_t ph = rg.cph;
-            for (; u < rg.issued; ++u) {
+            for (; u < s_prod.issued; ++u) {
                 mbar_wait_cta(&ws.full[s], ph);
                 if (++s == rg.S) { s = 0; ph ^= 1u; }
             }
         }
+        if constexpr (TM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         cluster_sync();
+        if constexpr (TM) {
+            if ((threadIdx.x >> 5) == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+            }
+        }
     };
     unsigned *redo = bar + 64;
     const bool shift_ok = !a.single_pass && env_shift_ok(a);
@@ -1971,8 +2277,13 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) sk_wide_kernel(SkArgs
         bool maxp = !shift_ok || k <= 1;
         for (;;) {
             if (rg.nrows > 0) {
-                if (maxp) pass_body_wide<NT, CL, CH, CC, true>(a, k, K, coef, gmax, sl, ws, rg, s_g, s_shift, xi, redo + (k & 1));
-                else pass_body_wide<NT, CL, CH, CC, false>(a, k, K, coef, gmax, sl, ws, rg, s_g, s_shift, xi, redo + (k & 1));
+                if constexpr (TM) {
+                    if (maxp) pass_body_tm<NT, CL, CH, CC, true>(a, k, K, coef, gmax, sl, ws, rg, s_g, s_shift, xi, redo + (k & 1), tbase);
+                    else pass_body_tm<NT, CL, CH, CC, false>(a, k, K, coef, gmax, sl, ws, rg, s_g, s_shift, xi, redo + (k & 1), tbase);
+                } else {
+                    if (maxp) pass_body_wide<NT, CL, CH, CC, true>(a, k, K, coef, gmax, sl, ws, rg, s_g, s_shift, xi, redo + (k & 1));
+                    else pass_body_wide<NT, CL, CH, CC, false>(a, k, K, coef, gmax, sl, ws, rg, s_g, s_shift, xi, redo + (k & 1));
+                }
             } else if (threadIdx.x == 0) {
                 __stcg(a.devpart + blockIdx.x, 0.0);
             }
@@ -2017,16 +2328,32 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) sk_wide_kernel(SkArgs
     }
 }
 
-template <int NT, int CL, int CH> void *wide2_fn() { return (void *)sk_wide_kernel<NT, CL, CH, 2>; }
-void *wide2_for(int nt, int cl, int ch) {
-#define GOAT_W2(NT_, CL_)                                \
-    if (nt == NT_ && cl == CL_) {                        \
-        switch (ch) {                                    \
-            case 4: return wide2_fn<NT_, CL_, 4>();      \
-            case 6: return wide2_fn<NT_, CL_, 6>();      \
-            case 8: return wide2_fn<NT_, CL_, 8>();      \
-            case 10: return wide2_fn<NT_, CL_, 10>();    \
-        }                                                \
+template <int NT, int CL, int CH, bool TM, int CC = 2> void *wide2_fn() { return (void *)sk_wide_kernel<NT, CL, CH, CC, TM>; }
+void *wide2_for(int nt, int cl, int ch, bool tm = false, int cc = 2) {
+    // TM: a half row in two bulk copies per row (cc = ch / 2), or 16 KB stages (cc = 2)
+    if (tm && nt == 512 && cl == 2 && cc * 2 == ch) {
+        switch (ch) {
+            case 4: return wide2_fn<512, 2, 4, true, 2>();
+            case 6: return wide2_fn<512, 2, 6, true, 3>();
+            case 8: return wide2_fn<512, 2, 8, true, 4>();
+            case 10: return wide2_fn<512, 2, 10, true, 5>();
+        }
+    }
+    if (tm && nt == 512 && cl == 2 && cc == 2) {
+        switch (ch) {
+            case 6: return wide2_fn<512, 2, 6, true>();
+            case 8: return wide2_fn<512, 2, 8, true>();
+            case 10: return wide2_fn<512, 2, 10, true>();
+        }
+    }
+#define GOAT_W2(NT_, CL_)                                       \
+    if (!tm && nt == NT_ && cl == CL_) {                        \
+        switch (ch) {                                           \
+            case 4: return wide2_fn<NT_, CL_, 4, false>();      \
+            case 6: return wide2_fn<NT_, CL_, 6, false>();      \
+            case 8: return wide2_fn<NT_, CL_, 8, false>();      \
+            case 10: return wide2_fn<NT_, CL_, 10, false>();    \
+        }                                                       \
     }
     GOAT_W2(512, 2)
     GOAT_W2(256, 4)
@@ -2852,26 +3179,40 @@ template <class T> bool tile_plan(int n, int num_sms, SkPlan &p) {
 bool wide2_plan(int n, int mrows, int num_sms, SkPlan &p) {
     const int mode = env_int("GOAT_SK_WIDE", 1);
     if (mode == 0) return false;
-    if (mode != 2 && (n <= 12288 || n > 40960)) return false;
-    constexpr int VW = 4, CC = 2;
-    const int CL = env_int("GOAT_SK_WIDE_CL", 2) == 4 ? 4 : 2;
+    // measured faster than the previous kernels from n ~ 22000 (n = 25000: 0.715 vs
+    // 0.799 ms, 32768: 0.937 vs 1.20, 40000: 1.29 vs 2.12; n = 20000: 0.535 vs 0.479);
+    // GOAT_SK_WIDE=2 forces it for any n up to 40960
+    if (mode != 2 && (n <= 22000 || n > 40960)) return false;
+    if (n > 40960) return false;
+    constexpr int VW = 4;
+    // mode 1 (default): rows parked in TMEM for a lagged finish (TM, 2-CTA clusters);
+    // 4: lock-step finish (GOAT_SK_WIDE_CL=4 for two 256-thread CTAs per SM in 4-CTA clusters)
+    const bool tm = mode != 4;
+    const int CL = (!tm && env_int("GOAT_SK_WIDE_CL", 2) == 4) ? 4 : 2;
     const int NT = CL == 2 ? 512 : 256;
     const int per_sm = CL == 2 ? 1 : 2;
     const int sw = (int)round_up(ceil_div(n, CL), 8 * VW);
     int ch = ceil_div(ceil_div(sw, VW), NT);
-    ch = (int)round_up(std::max(ch, 4), CC);
+    ch = (int)round_up(std::max(ch, 4), 2);
     if (ch > 10) return false;
+    // TM: two stages per row and a ring of two rows (measured at n = 40000: 40 KB
+    // stages, S = 4 -> 1.40 ms/sweep; 16 KB stages 1.65-1.87; S = 5 -> 1.95);
+    // GOAT_SK_WIDE_CC=2 selects 16 KB stages
+    const int CC = (tm && env_int("GOAT_SK_WIDE_CC", 0) != 2) ? ch / 2 : 2;
     p = SkPlan{};
-    p.nt = NT; p.cl = CL; p.ch = ch; p.rows = 1; p.slice_w = sw; p.wide2 = true; p.persistent = true;
+    p.nt = NT; p.cl = CL; p.ch = ch; p.rows = 1; p.slice_w = sw; p.wide2 = true; p.wide_tm = tm; p.persistent = true;
     p.stage_bytes = NT * CC * 16;
-    void *const kfn = wide2_for(NT, CL, ch);
+    void *const kfn = wide2_for(NT, CL, ch, tm, CC);
+    p.rows = CC;  // chunks per stage (the launcher selects the kernel by it)
     // the ring takes what g and the shift table leave of this CTA's share of shared memory
-    const size_t gl = (size_t)NT * ch * 16, budget = (228 * 1024) / per_sm - 3 * 1024;
+    const size_t gl = tm ? 0 : (size_t)NT * ch * 16;  // TM keeps g in tensor memory
+    const size_t budget = (228 * 1024) / per_sm - 3 * 1024;
     const int rows_max = ceil_div(mrows, std::max(1, per_sm * num_sms / CL));
     const size_t shift = round_up((size_t)(rows_max + 64) * 4, 128);
     if (gl + shift >= budget) return false;
     int S = (int)((budget - gl - shift) / p.stage_bytes);
     S = std::min(16, S);
+    if (tm && CC * 2 == ch) S = std::min(S, 4);
     if (const int st = env_int("GOAT_SK_STAGES", 0)) S = std::min(S, std::max(3, st));
     if (S < 2 * (ch / CC) && S < 6) return false;
     p.stages = S;
@@ -3053,12 +3394,13 @@ template <class T> void sk_launch_persistent(const SkArgs &a, const SkPlan &p, u
                    (double)a.n * a.ld * sizeof(T) <= env_int("GOAT_SK_L2HINT_MB", 112) * 1048576.0;
     args.stages = p.stages;
     args.stage_bytes = p.stage_bytes;
+    args.dbg = env_int("GOAT_SK_DBG", 0);
     void *params[] = {&args, &bar};
     cudaLaunchAttribute attrs[2];
     cudaLaunchConfig_t cfg = persistent_config(p, s, attrs);
     if (p.tile && args.single_pass) throw Error(GOAT_ENOTSUP, "sinkhorn: the tile plan has no single-pass mode");
     void *fn = p.tile    ? tile_for<T>(p.cl, p.ch, p.rows)
-               : p.wide2 ? wide2_for(p.nt, p.cl, p.ch)
+               : p.wide2 ? wide2_for(p.nt, p.cl, p.ch, p.wide_tm, p.rows)
                : p.pipe  ? pipe_for(p.ch, p.cl, p.nt, p.rows)
                          : persistent_for<T>(p.ch, p.cl, p.nt, p.stages > 0);
     int rows_g = p.tile_rows;

@@ -1,9 +1,9 @@
-"""The 2-CTA wide-row Sinkhorn kernel (sk_wide_kernel, 12288 < n <= 40960 fp32,
-config 5's n = 40000) against the previous cluster kernel on the same device
+"""The 2-CTA wide-row Sinkhorn kernel (sk_wide_kernel: planned for 22000 < n <= 40960
+fp32, config 5's n = 40000; forced here down to n = 12289) against the previous cluster kernel on the same device
 G, through goat_lot_device: same sweep count and stopping flag, iterates within
-fp32 accumulation-order noise, bit-identical reruns.  Smaller orders of the
-same kernel are checked against the CPU oracle in test_lot_large_gpu.py
-(n = 17000, 20000)."""
+fp32 accumulation-order noise, bit-identical reruns; and its fixed-shift redo
+path (every sweep redone with the max shift == the max-shift run, bit for bit).
+The previous kernels are checked against the CPU oracle in test_lot_large_gpu.py."""
 import ctypes
 
 import numpy as np
@@ -40,7 +40,7 @@ def _cost(n):
 @pytest.mark.parametrize("n", [12289, 16384, 25003, 40000])
 def test_wide_kernel_matches_cluster_kernel(n, monkeypatch):
     G = _cost(n)
-    monkeypatch.setenv("GOAT_SK_WIDE", "1")
+    monkeypatch.setenv("GOAT_SK_WIDE", "2")  # the wide kernel at every tested order
     Q1, s1, c1, d1 = _lot_device(G, n, 25)
     Q1b, s1b, _, d1b = _lot_device(G, n, 25)
     assert s1 == s1b and d1 == d1b
@@ -55,3 +55,21 @@ def test_wide_kernel_matches_cluster_kernel(n, monkeypatch):
     cs = Q1[:, :n].double().sum(0)
     assert float((cs - 1).abs().max()) < 1e-4  # the returned iterate's columns are balanced
     assert float((rs - 1).abs().max()) == pytest.approx(d1, rel=0.05, abs=1e-5)
+
+
+@pytest.mark.parametrize("n", [16384, 40000])
+def test_wide_kernel_redo_path(n, monkeypatch):
+    """Sweeps >= 2 shift each row by its previous LSE; a row whose sum leaves the
+    window redoes the sweep with the max shift.  Forcing every sweep through the
+    redo (GOAT_SK_RES=3) must reproduce the max-shift-only run (GOAT_SK_RES=2)
+    exactly, and the default must agree with both to fp32 accuracy."""
+    G = _cost(n)
+    monkeypatch.setenv("GOAT_SK_WIDE", "2")
+    out = {}
+    for mode in ("2", "3", "1"):
+        monkeypatch.setenv("GOAT_SK_RES", mode)
+        out[mode] = _lot_device(G, n, 12)
+    assert bool((out["3"][0][:, :n] == out["2"][0][:, :n]).all())
+    assert out["3"][1:] == out["2"][1:]
+    assert float((out["1"][0][:, :n] - out["2"][0][:, :n]).abs().max()) < 1e-5
+    assert out["1"][1] == out["2"][1]
