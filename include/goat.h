@@ -85,6 +85,8 @@ typedef struct goat_fw_result {
     int32_t gpu_launches;    /* out: kernels launched by this call */
     double objective;        /* out: sum_ij A_ij B_{p(i)p(j)} on the inputs (core.py:120-124) */
     double time_ms[6];       /* out: gradient, lot, linesearch+update, lap, h2d+setup, total */
+    int32_t *lot_fp64_from;  /* [max_iters] out or NULL: fp32 handles, sweeps done in fp32 before the LOT
+                              * finished in fp64 arithmetic (-1: the whole LOT ran in the handle's precision) */
 } goat_fw_result;
 
 int goat_create(goat_handle **out, const goat_config *cfg);

@@ -10,12 +10,15 @@ no CPU fallback.
 """
 
 from .engine import fw_core, frank_wolfe_match, seeded_match
-from .graphs import correlated_er_pair, correlated_sbm_pair, shuffle as _shuffle
+from .formats import (format_matrix_text, format_permutation_text, parse_matrix_text,
+                      parse_permutation_text, pass_to_ranks)
+from .graphs import (SbmSpec, correlated_er_pair, correlated_sbm_pair, replicate_rng, sample_sbm_pair,
+                     shuffle as _shuffle)
 from .matrices import (DS_TOL, as_doubly_stochastic, as_permutation, as_square_matrix,
                        barycenter, compose_permutations, edge_disagreements,
                        invert_permutation, match_ratio, permutation_matrix, permute_matrix,
                        qap_objective)
-from .ops import (exact_line_search, gradient, lot, random_doubly_stochastic,
+from .ops import (exact_line_search, gradient, lap_tie_set, lot, random_doubly_stochastic,
                   randomized_blend_init, sinkhorn_knopp, solve_lap)
 from .records import (LapSolution, MatchOptions, MatchResult, SeedSet, SinkhornParams,
                       SinkhornResult)
@@ -40,5 +43,7 @@ __all__ = [
     "exact_line_search", "frank_wolfe_match", "fw_core", "gradient", "invert_permutation",
     "lot", "match_ratio", "permutation_matrix", "permute_matrix", "qap_objective",
     "random_doubly_stochastic", "randomized_blend_init", "sample_er_pair", "seeded_match",
-    "shuffle_pair", "sinkhorn_knopp", "solve_lap",
+    "shuffle_pair", "sinkhorn_knopp", "solve_lap", "SbmSpec", "sample_sbm_pair", "replicate_rng",
+    "lap_tie_set", "pass_to_ranks", "parse_matrix_text", "format_matrix_text", "parse_permutation_text",
+    "format_permutation_text",
 ]

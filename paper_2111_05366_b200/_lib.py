@@ -45,7 +45,8 @@ class GoatFwResult(ctypes.Structure):
                 ("lot_converged", _c_i32_p), ("lot_dev", _c_double_p),
                 ("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
                 ("lap_certified", ctypes.c_int32), ("gpu_launches", ctypes.c_int32),
-                ("objective", ctypes.c_double), ("time_ms", ctypes.c_double * 6)]
+                ("objective", ctypes.c_double), ("time_ms", ctypes.c_double * 6),
+                ("lot_fp64_from", _c_i32_p)]
 
 
 class GoatCsr(ctypes.Structure):
@@ -227,6 +228,14 @@ def handle(device=0, precision="fp64", gemm="auto") -> Handle:
             h = Handle(device, precision, gemm)
             _handles[key] = h
         return h
+
+
+def release_handles() -> None:
+    """Destroy this process's cached handles (frees their device workspace)."""
+    with _handles_lock:
+        for h in _handles.values():
+            h.close()
+        _handles.clear()
 
 
 def stream_handle(torch_stream) -> ctypes.c_void_p:

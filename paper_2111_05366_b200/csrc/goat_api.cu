@@ -41,7 +41,7 @@ struct Handle {
     int64_t cap_n = 0;    // vectors / scratch sized for this order
     int64_t cap_mat = 0;  // n x n workspace sized for this order
     DevBuf A, B, P, Q, G, GQ, T1, L, Gl, M;     // element = precision
-    DevBuf A64, B64, stage;                     // fp64 inputs (objective) + upload staging
+    DevBuf A64, B64, G64, stage;                     // fp64 inputs (objective) + upload staging
     DevBuf f[2], g[2], colpart, devpart, devcol, state, red, scal, vec, ivec;
     DevBuf lap_d[3], lap_i[4], lap_b[2], lap_misc, bar;
     DevBuf auc_d[2], auc_i[4], auc_u64, auc_misc;  // auction LAP state
@@ -394,7 +394,42 @@ struct LotOut {
     double nrm = 0.0;  // sum (Q - P)^2 (when P given)
     double lq = 0.0;   // <L, Q> (when L given)
     bool used_kernel = true;
+    int fp64_from = -1;  // fp32 handles: sweeps done in fp32 before the fp64 finish (-1: none)
 };
+
+// Sweeps in fp32 arithmetic stop at this marginal deviation; below it an fp32
+// handle finishes the LOT in fp64 arithmetic (run_lot).  GOAT_SK_FP64_FINISH=0
+// keeps the pure-fp32 loop (measurement only: it cannot meet tol < floor).
+constexpr double kFp32DevFloor = 1e-4;
+inline bool fp64_finish_enabled() {
+    const char *e = getenv("GOAT_SK_FP64_FINISH");
+    return !(e && atoi(e) == 0);
+}
+
+// Runs the sweep loop from the device state (SkState.k .. stop) and leaves the
+// final state in h.h_state.
+template <class U>
+void run_sweeps(Ctx &c, const SkArgs &a, const SkPlan &plan, int max_sweeps) {
+    Handle &h = c.h;
+    if (plan.persistent) {
+        sk_launch_persistent<U>(a, plan, h.bar.as<unsigned>(), c.s);
+    } else {
+        const int max_passes = max_sweeps + 2;
+        const int poll = 8;
+        for (int p = 0; p < max_passes; ++p) {
+            sk_launch_pass<U>(a, plan, c.s);
+            sk_launch_merge<U>(a, plan, c.s);
+            if ((p + 1) % poll == 0 || p + 1 == max_passes) {
+                GOAT_CUDA(cudaMemcpyAsync(h.h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost, c.s));
+                sync(c);
+                if (h.h_state->done) break;
+            }
+        }
+    }
+    GOAT_CUDA(cudaMemcpyAsync(h.h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    if (!h.h_state->done) throw Error(GOAT_ECUDA, "sinkhorn loop did not terminate");
+}
 
 // mode: 0 = lot(M) (sinkhorn.py:103-130); 1 = sinkhorn_knopp on K = exp(-Gin)
 template <class T>
@@ -437,29 +472,43 @@ LotOut run_lot(Ctx &c, const T *Gin, int sense, double lam, int max_sweeps, doub
     a.st = h.state.as<SkState>(); a.nblk = plan.nblk;
     GOAT_CUDA(cudaMemsetAsync(a.f[0], 0, c.ld * 8, c.s));
     GOAT_CUDA(cudaMemsetAsync(a.g[0], 0, c.ld * 8, c.s));
+    // fp32 arithmetic resolves the marginal deviation |u K v - 1| only down to
+    // ~1e-5 (exponent rounding at |E + f + g| ~ 1e2), so a tolerance below
+    // kFp32DevFloor (the default 1e-8, sinkhorn.py:32) can never fire and every LOT
+    // would run max_sweeps.  fp32 handles therefore sweep in fp32 down to the
+    // floor and finish in fp64 arithmetic on the same (exactly widened) fp32 G
+    // from the same potentials, which restores the reference's stopping rule.
+    const bool finish64 = sizeof(T) == 4 && tol < kFp32DevFloor && fp64_finish_enabled();
     SkState st0{};
     st0.k = log_mode ? 1 : 0;
-    st0.gmax = gmax; st0.coef = coef; st0.tol = tol; st0.max_sweeps = max_sweeps; st0.log_mode = log_mode;
+    st0.gmax = gmax; st0.coef = coef; st0.tol = finish64 ? kFp32DevFloor : tol;
+    st0.max_sweeps = max_sweeps; st0.log_mode = log_mode;
     *h.h_state = st0;
     GOAT_CUDA(cudaMemcpyAsync(a.st, h.h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
-    if (plan.persistent) {
-        sk_launch_persistent<T>(a, plan, h.bar.as<unsigned>(), c.s);
-    } else {
-        const int max_passes = max_sweeps + 2;
-        const int poll = 8;
-        for (int p = 0; p < max_passes; ++p) {
-            sk_launch_pass<T>(a, plan, c.s);
-            sk_launch_merge<T>(a, plan, c.s);
-            if ((p + 1) % poll == 0 || p + 1 == max_passes) {
-                GOAT_CUDA(cudaMemcpyAsync(h.h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost, c.s));
-                sync(c);
-                if (h.h_state->done) break;
-            }
+    run_sweeps<T>(c, a, plan, max_sweeps);
+    if constexpr (sizeof(T) == 4) if (finish64 && h.h_state->converged) {
+        // stopped at the floor after pass k = sweeps + 1: redo that pass and go on
+        // in fp64 (sweeps == 0: the marginal pre-check itself, redone from scratch)
+        const int swept = h.h_state->sweeps;
+        h.G64.ensure((size_t)n * c.ld * sizeof(double));
+        launch_convert_to_f64<T>(Gin, c.ld, h.G64.as<double>(), c.ld, n, c.s);
+        SkPlan plan64 = sk_plan<double>(n, h.num_sms);
+        h.colpart.ensure(plan64.colpart_bytes);
+        SkArgs a64 = a;
+        a64.G = h.G64.p; a64.colpart = h.colpart.p; a64.nblk = plan64.nblk;
+        a.colpart = h.colpart.p;
+        SkState st1 = st0;
+        st1.tol = tol;
+        if (swept > 0) st1.k = swept + 1;
+        else {
+            GOAT_CUDA(cudaMemsetAsync(a.f[0], 0, c.ld * 8, c.s));
+            GOAT_CUDA(cudaMemsetAsync(a.g[0], 0, c.ld * 8, c.s));
         }
+        *h.h_state = st1;
+        GOAT_CUDA(cudaMemcpyAsync(a.st, h.h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
+        run_sweeps<double>(c, a64, plan64, max_sweeps);
+        out.fp64_from = swept;
     }
-    GOAT_CUDA(cudaMemcpyAsync(h.h_state, a.st, sizeof(SkState), cudaMemcpyDeviceToHost, c.s));
-    sync(c);
-    if (!h.h_state->done) throw Error(GOAT_ECUDA, "sinkhorn loop did not terminate");
     out.sweeps = h.h_state->sweeps;
     out.converged = h.h_state->converged;
     out.dev = h.h_state->dev;
@@ -641,6 +690,7 @@ void fw_loop(Ctx &c, bool have_L, bool p0_bary, const goat_options &o, goat_fw_r
         if (res->lot_sweeps) res->lot_sweeps[i - 1] = lo.sweeps;
         if (res->lot_converged) res->lot_converged[i - 1] = lo.converged;
         if (res->lot_dev) res->lot_dev[i - 1] = lo.dev;
+        if (res->lot_fp64_from) res->lot_fp64_from[i - 1] = lo.fp64_from;
         {
             Timer tm(c.s);
             gradient<T>(c, A, B, Q, GQ, T1);

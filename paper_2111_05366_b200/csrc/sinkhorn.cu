@@ -2763,6 +2763,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
         gsl[c] = gv;
         gst[c] = ok ? (T)(gv * ks) : neg_inf<T>();
     }
+    // a LOT resumed at pass k0 >= 2 (the fp64 finish of an fp32 handle): f_{k0-1}
+    for (int r = tid; r < rows_g; r += kTileThreads)
+        fpr[r] = (k0 >= 2 && r < nr) ? __ldcg(fslot(a, k0 + 1) + r0 + r) : 0.0;
     if (tid == 0) {
         xbar_init(&xbar[0]);
         xbar_init(&xbar[1]);

@@ -19,6 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = [
+    "SbmSpec", "sample_sbm_pair", "replicate_rng",
     "correlated_sbm_pair", "correlated_er_pair", "directed_er_pair",
     "weighted_directed_pair", "shuffle", "relabel", "CsrGraph",
     "sparse_er_pair_csr", "config_pair", "CONFIGS",
@@ -49,6 +50,46 @@ def correlated_sbm_pair(block_sizes, block_probs, rho, rng):
         M[lo] = 0.0
         M[(iu[1], iu[0])] = M[iu]
     return A, B
+
+
+@dataclass(frozen=True)
+class SbmSpec:
+    """Block sizes, symmetric block edge probabilities and edge correlation of a
+    correlated SBM (samplers.py:17-46; same validation and ValueErrors)."""
+
+    block_sizes: tuple
+    block_probs: np.ndarray
+    rho: float
+
+    def __post_init__(self):
+        sizes = tuple(int(b) for b in self.block_sizes)
+        if len(sizes) == 0 or min(sizes) < 1:
+            raise ValueError("block_sizes must be positive integers")
+        probs = np.asarray(self.block_probs, dtype=float)
+        if probs.shape != (len(sizes), len(sizes)):
+            raise ValueError(f"block_probs must be {len(sizes)}x{len(sizes)}, got {probs.shape}")
+        if not np.allclose(probs, probs.T):
+            raise ValueError("block_probs must be symmetric")
+        if probs.min() < 0 or probs.max() > 1:
+            raise ValueError("block_probs entries must lie in [0, 1]")
+        if not 0.0 <= self.rho <= 1.0:
+            raise ValueError("rho must lie in [0, 1]")
+        object.__setattr__(self, "block_sizes", sizes)
+        object.__setattr__(self, "block_probs", probs)
+
+    @property
+    def n(self) -> int:
+        return sum(self.block_sizes)
+
+
+def sample_sbm_pair(spec: SbmSpec, rng):
+    """rho-correlated SBM pair with identity correspondence (samplers.py:48-72)."""
+    return correlated_sbm_pair(spec.block_sizes, spec.block_probs, spec.rho, rng)
+
+
+def replicate_rng(master_seed: int, replicate: int):
+    """Independent deterministic stream of one replicate (samplers.py:92-94)."""
+    return np.random.default_rng([master_seed, replicate])
 
 
 def correlated_er_pair(n, p, rho, rng):

@@ -155,6 +155,31 @@ def solve_lap(M, sense: str = "minimize", *, device=0, precision="fp64") -> LapS
     return LapSolution(assignment=p, objective=float(M[np.arange(n), p].sum()))
 
 
+#: largest order accepted by the exhaustive tie enumeration (lap.py:22)
+TIE_SET_MAX_N = 10
+
+
+def lap_tie_set(M, sense: str = "minimize", atol: float = 1e-9, *, device=0, precision="fp64") -> list:
+    """Every permutation within ``atol`` of the LAP optimum (lap.py:61-80): the
+    optimum from the device solver, then exhaustive enumeration (n <= 10)."""
+    import itertools
+
+    M = as_square_matrix(M, "M")
+    if sense not in SENSES:
+        raise ValueError(f"sense must be one of {SENSES}, got {sense!r}")
+    n = M.shape[0]
+    if n > TIE_SET_MAX_N:
+        raise ValueError(f"lap_tie_set is exhaustive; n = {n} exceeds {TIE_SET_MAX_N}")
+    best = solve_lap(M, sense, device=device, precision=precision).objective
+    rows = np.arange(n)
+    out = []
+    for cand in itertools.permutations(range(n)):
+        q = np.array(cand, dtype=np.intp)
+        if abs(float(M[rows, q].sum()) - best) <= atol:
+            out.append(q)
+    return out
+
+
 def random_doubly_stochastic(n: int, rng: np.random.Generator, *, device=0,
                              precision="fp64") -> np.ndarray:
     """Uniform(0,1) matrix (host RNG stream) balanced on the device (matcher.py:157-162)."""

@@ -45,6 +45,30 @@ def test_oracle_fw_matches_reference(case):
             np.testing.assert_allclose(q_o, q_r, atol=1e-14)
 
 
+FAQ = Fixture("faq_cases.npz")
+
+
+@pytest.mark.parametrize("case", ["faq_w150", "faq_w150_min", "faq_w300"])
+def test_oracle_faq_matches_reference(case):
+    """FAQ branch (exact LAP steps, matcher.py:191-192) on tie-free weighted graphs
+    (tests/golden/make_faq_golden.py): the oracle follows the reference exactly."""
+    import hashlib
+
+    from paper_2111_05366_b200 import graphs
+    rep, n, smax, mi = (int(x) for x in FAQ[f"{case}/spec"])
+    A, B, _ = graphs.config_pair(4, rep, n=n)
+    for M, tag in ((A, "A"), (B, "B")):
+        assert hashlib.sha256(np.ascontiguousarray(M).tobytes()).hexdigest() == str(FAQ[f"{case}/sha_{tag}"])
+    align, obj, iters, hist, conv = O.run_seeded(
+        A, B, np.empty((0, 2), dtype=np.int64), step_solver="exact_lap",
+        sense="maximize" if smax else "minimize", max_iters=mi)
+    np.testing.assert_array_equal(align, FAQ[f"{case}/alignment"])
+    assert obj == FAQ[f"{case}/objective"]
+    assert iters == int(FAQ[f"{case}/iterations"]) and conv == bool(FAQ[f"{case}/converged"])
+    alphas = np.array([np.nan if h[2] is None else h[2] for h in hist])
+    np.testing.assert_allclose(alphas, FAQ[f"{case}/hist_alpha"], rtol=1e-12, atol=1e-15)
+
+
 @pytest.mark.parametrize("name", list(UNIT["lot/names"]))
 def test_oracle_lot_matches_reference(name):
     M = UNIT[f"lot/{name}/M"]

@@ -71,7 +71,7 @@ def test_fw_fp64_matches_reference(case):
 
 
 FP32_CASES = ["c1_r0", "c1_r1", "c1_r2", "c1_r3", "c1_r4", "c2_r0", "c2_r1", "iso200_r0",
-              "iso200_r1", "iso200_r2", "c4s_r0"]
+              "iso200_r1", "iso200_r2", "c4s_r0", "c3s_r0", "c5p_r0"]
 
 
 @pytest.mark.parametrize("case", FP32_CASES)
@@ -104,6 +104,35 @@ def test_faq_exact_lap_step():
     objs = [o for _, o, _ in res.iterate_history]
     assert all(b >= a - 1e-9 for a, b in zip(objs, objs[1:]))
     assert res.objective == pytest.approx(float(FW[f"{case}/objective"]), rel=0.05)
+
+
+FAQ = Fixture("faq_cases.npz")
+
+
+@pytest.mark.parametrize("case", ["faq_w150", "faq_w150_min", "faq_w300", "faq_w700"])
+def test_faq_exact_parity_on_tie_free_graphs(case):
+    """FAQ with every step on the device LAP (matcher.py:191-192, lap.py:48-58)
+    against the UNMODIFIED reference on weighted graphs, whose gradients never tie
+    (tests/golden/make_faq_golden.py): the same permutation, objective, iteration
+    count, convergence flag and alpha sequence.  n = 150 runs the scipy-order
+    augmenting-path solver, n >= 256 the auction + certified repair."""
+    import hashlib
+
+    from paper_2111_05366_b200 import graphs
+    rep, n, smax, mi = (int(x) for x in FAQ[f"{case}/spec"])
+    A, B, _ = graphs.config_pair(4, rep, n=n)
+    for M, tag in ((A, "A"), (B, "B")):
+        assert hashlib.sha256(np.ascontiguousarray(M).tobytes()).hexdigest() == str(FAQ[f"{case}/sha_{tag}"])
+    res = gb.frank_wolfe_match(A, B, gb.MatchOptions(
+        step_solver="exact_lap", objective_sense="maximize" if smax else "minimize", max_iters=mi,
+        precision="fp64"))
+    np.testing.assert_array_equal(res.alignment, FAQ[f"{case}/alignment"])
+    assert res.objective == pytest.approx(float(FAQ[f"{case}/objective"]), rel=1e-12)
+    assert res.iterations == int(FAQ[f"{case}/iterations"])
+    assert res.converged == bool(FAQ[f"{case}/converged"])
+    ours = np.array([np.nan if h[2] is None else h[2] for h in res.iterate_history])
+    np.testing.assert_allclose(ours, FAQ[f"{case}/hist_alpha"], atol=1e-9)
+    np.testing.assert_allclose([h[1] for h in res.iterate_history], FAQ[f"{case}/hist_obj"], rtol=1e-10)
 
 
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
