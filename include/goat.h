@@ -251,6 +251,11 @@ int goat_shard_lot_repair_merge(goat_handle *h, const double *dRecvPairs, int32_
  * repair round pending. */
 int goat_shard_lot_status(goat_handle *h, int32_t *done, int32_t *sweeps, int32_t *converged,
                           double *deviation, int32_t *repaired, int32_t *pending);
+/* fp32 handles: once the fp32 sweeps have stopped at the fp32 deviation floor (tol
+ * below it), widen the block to fp64 and re-open the loop so passes/merges go on
+ * in fp64 arithmetic from the same potentials (*started = 1); otherwise a no-op
+ * (*started = 0).  Identical decision on every rank (the loop state is). */
+int goat_shard_lot_refine(goat_handle *h, const void *dG_rows, int32_t *started);
 /* Q_r = exp(E + f + g) of the returned iterate (1/n when the cost was constant). */
 int goat_shard_lot_emit(goat_handle *h, const void *dG_rows, void *dQ_rows);
 /* local line-search sums of goat_fw_core's dots: <GQ,D>, <GP-GQ,D>, <GQ,Q>, |D|^2, 0, 0 (D = P - Q). */

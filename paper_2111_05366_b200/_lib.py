@@ -132,6 +132,7 @@ def _bind(lib):
         "goat_shard_lot_merge": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_int32]),
         "goat_shard_lot_status": (ctypes.c_int, [H, _c_i32_p, _c_i32_p, _c_i32_p, _c_double_p, _c_i32_p,
                                                  _c_i32_p]),
+        "goat_shard_lot_refine": (ctypes.c_int, [H, ctypes.c_void_p, _c_i32_p]),
         "goat_shard_lot_repair_pass": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_void_p]),
         "goat_shard_lot_repair_merge": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_int32]),
         "goat_shard_lot_emit": (ctypes.c_int, [H, ctypes.c_void_p, ctypes.c_void_p]),
@@ -156,7 +157,7 @@ EXPORTS = ("goat_create", "goat_destroy", "goat_last_error", "goat_version", "go
            "goat_qap_objective_perm", "goat_set_stream", "goat_bench_sweep",
            "goat_bench_gradient", "goat_lap_device", "goat_shard_setup", "goat_shard_setup_csr", "goat_shard_gradient",
            "goat_shard_minmax", "goat_shard_lot_begin", "goat_shard_lot_pass", "goat_shard_lot_merge",
-           "goat_shard_lot_status", "goat_shard_lot_repair_pass", "goat_shard_lot_repair_merge",
+           "goat_shard_lot_status", "goat_shard_lot_refine", "goat_shard_lot_repair_pass", "goat_shard_lot_repair_merge",
            "goat_shard_lot_emit", "goat_shard_dots", "goat_shard_axpby",
            "goat_shard_fill")
 

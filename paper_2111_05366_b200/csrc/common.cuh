@@ -81,6 +81,7 @@ struct SkState {
     int log_mode;
     double dcol;    // row-sharded pre-check: column deviation of the columns that needed no repair
     int redone;     // wide fp32 rows: sweeps recomputed with the max shift (diagnostic)
+    int nostop_k;   // a resumed LOT: the convergence test may not fire at passes <= nostop_k (0 = none)
 };
 
 // Count of kernels this library launched (reported as gpu_launches).

@@ -59,6 +59,12 @@ struct Handle {
         SkPlan plan;
         DevBuf bad;               // per-column repair flags of the current sweep
         bool csr = false;         // gradient by SpMM on CSR rows (goat_shard_setup_csr)
+        // fp32 handles: the LOT finishes in fp64 arithmetic below the fp32 deviation floor
+        // (goat_shard_lot_refine; same rule as run_lot)
+        double user_tol = 0.0;
+        bool phase64 = false;
+        SkPlan plan64;
+        DevBuf G64;
     } sh;
     // sparse (CSR) adjacency: A, A^T, B, B^T (goat_fw_core_csr*); values null = 0/1
     struct Csr {
@@ -487,8 +493,13 @@ LotOut run_lot(Ctx &c, const T *Gin, int sense, double lam, int max_sweeps, doub
     GOAT_CUDA(cudaMemcpyAsync(a.st, h.h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
     run_sweeps<T>(c, a, plan, max_sweeps);
     if constexpr (sizeof(T) == 4) if (finish64 && h.h_state->converged) {
-        // stopped at the floor after pass k = sweeps + 1: redo that pass and go on
-        // in fp64 (sweeps == 0: the marginal pre-check itself, redone from scratch)
+        // Stopped at the floor at pass k = sweeps + 1 (which produced f_k and
+        // dev_{k-1} in fp32).  The fp64 loop re-enters one pass earlier: pass k-1
+        // recomputes f_{k-1} and g_{k-1} in fp64 from g_{k-2} (still in its ring
+        // slot: pass k never merged), so the first deviation it may act on, dev_{k-1}
+        // at pass k, compares two fp64 row sums.  The re-entry pass itself cannot
+        // stop (its f_{k-2} slot was overwritten).  sweeps == 0: the marginal
+        // pre-check fired, redone from scratch.
         const int swept = h.h_state->sweeps;
         h.G64.ensure((size_t)n * c.ld * sizeof(double));
         launch_convert_to_f64<T>(Gin, c.ld, h.G64.as<double>(), c.ld, n, c.s);
@@ -499,7 +510,7 @@ LotOut run_lot(Ctx &c, const T *Gin, int sense, double lam, int max_sweeps, doub
         a.colpart = h.colpart.p;
         SkState st1 = st0;
         st1.tol = tol;
-        if (swept > 0) st1.k = swept + 1;
+        if (swept > 0) { st1.k = swept; st1.nostop_k = swept; }
         else {
             GOAT_CUDA(cudaMemsetAsync(a.f[0], 0, c.ld * 8, c.s));
             GOAT_CUDA(cudaMemsetAsync(a.g[0], 0, c.ld * 8, c.s));
@@ -1684,9 +1695,12 @@ int goat_shard_lot_begin(goat_handle *h, int32_t sense, double lam, double gmin,
             st0.coef = maximize ? -lam / scale : lam / scale;
             st0.log_mode = !(std::exp((-lam / scale) * scale) > 0.0);
             st0.k = st0.log_mode ? 1 : 0;
-            st0.tol = tol;
+            const bool finish64 = h->precision == GOAT_FP32 && tol < kFp32DevFloor && fp64_finish_enabled();
+            st0.tol = finish64 ? kFp32DevFloor : tol;
             st0.max_sweeps = max_sweeps;
         }
+        S.user_tol = tol;
+        S.phase64 = false;
         const int64_t lw = ld_for(S.n);
         GOAT_CUDA(cudaMemsetAsync(h->f[0].p, 0, lw * 8, h->stream));
         GOAT_CUDA(cudaMemsetAsync(h->g[0].p, 0, lw * 8, h->stream));
@@ -1699,6 +1713,12 @@ int goat_shard_lot_pass(goat_handle *h, const void *dG_rows, double *dSend) {
     return guarded([&] {
         auto &S = shard_of(h);
         require(dG_rows && dSend, "NULL argument");
+        if (S.phase64) {
+            SkArgs a = shard_sk_args<double>(*h, S.G64.p);
+            a.nblk = S.plan64.nblk;
+            sk_launch_shard_pass<double>(a, S.plan64, h->bar.as<unsigned>(), dSend, h->stream);
+            return;
+        }
         dispatch(*h, [&](auto *tag) {
             using T = std::remove_pointer_t<decltype(tag)>;
             SkArgs a = shard_sk_args<T>(*h, dG_rows);
@@ -1709,8 +1729,13 @@ int goat_shard_lot_pass(goat_handle *h, const void *dG_rows, double *dSend) {
 
 int goat_shard_lot_merge(goat_handle *h, const double *dRecv, int32_t world) {
     return guarded([&] {
-        shard_of(h);
+        auto &S = shard_of(h);
         require(dRecv && world >= 1, "bad argument");
+        if (S.phase64) {
+            SkArgs a = shard_sk_args<double>(*h, nullptr);
+            sk_launch_shard_merge<double>(a, dRecv, world, S.bad.as<unsigned char>(), h->stream);
+            return;
+        }
         dispatch(*h, [&](auto *tag) {
             using T = std::remove_pointer_t<decltype(tag)>;
             SkArgs a = shard_sk_args<T>(*h, nullptr);
@@ -1721,8 +1746,13 @@ int goat_shard_lot_merge(goat_handle *h, const double *dRecv, int32_t world) {
 
 int goat_shard_lot_repair_pass(goat_handle *h, const void *dG_rows, double *dPairs) {
     return guarded([&] {
-        shard_of(h);
+        auto &S = shard_of(h);
         require(dG_rows && dPairs, "NULL argument");
+        if (S.phase64) {
+            SkArgs a = shard_sk_args<double>(*h, S.G64.p);
+            sk_launch_shard_repair_pass<double>(a, S.bad.as<unsigned char>(), dPairs, h->stream);
+            return;
+        }
         dispatch(*h, [&](auto *tag) {
             using T = std::remove_pointer_t<decltype(tag)>;
             SkArgs a = shard_sk_args<T>(*h, dG_rows);
@@ -1740,6 +1770,39 @@ int goat_shard_lot_repair_merge(goat_handle *h, const double *dRecvPairs, int32_
             SkArgs a = shard_sk_args<T>(*h, nullptr);
             sk_launch_shard_repair_merge(a, dRecvPairs, world, h->sh.bad.as<unsigned char>(), h->stream);
         });
+    });
+}
+
+int goat_shard_lot_refine(goat_handle *h, const void *dG_rows, int32_t *started) {
+    return guarded([&] {
+        auto &S = shard_of(h);
+        require(dG_rows && started, "NULL argument");
+        *started = 0;
+        if (h->precision != GOAT_FP32 || S.fill || S.phase64) return;
+        GOAT_CUDA(cudaMemcpyAsync(h->h_state, h->state.p, sizeof(SkState), cudaMemcpyDeviceToHost, h->stream));
+        GOAT_CUDA(cudaStreamSynchronize(h->stream));
+        SkState st = *h->h_state;
+        // the fp32 sweeps stopped at the floor (run_lot: same re-entry rule)
+        if (!(st.done && st.converged && S.user_tol < st.tol)) return;
+        const int64_t ld = ld_for(S.n);
+        S.G64.ensure((size_t)S.m * ld * sizeof(double));
+        launch_convert_to_f64<float>(static_cast<const float *>(dG_rows), ld, S.G64.as<double>(), ld, (int)S.n,
+                                     h->stream, (int)S.m);
+        S.plan64 = sk_plan<double>((int)S.n, h->num_sms, (int)S.m, true);
+        h->colpart.ensure(S.plan64.colpart_bytes);
+        const int swept = st.sweeps;
+        st.done = 0; st.converged = 0; st.pending = 0; st.tol = S.user_tol;
+        if (swept > 0) { st.k = swept; st.nostop_k = swept; }
+        else {
+            st.k = st.log_mode ? 1 : 0;
+            GOAT_CUDA(cudaMemsetAsync(h->f[0].p, 0, ld * 8, h->stream));
+            GOAT_CUDA(cudaMemsetAsync(h->g[0].p, 0, ld * 8, h->stream));
+        }
+        *h->h_state = st;
+        GOAT_CUDA(cudaMemcpyAsync(h->state.p, h->h_state, sizeof(SkState), cudaMemcpyHostToDevice, h->stream));
+        GOAT_CUDA(cudaStreamSynchronize(h->stream));
+        S.phase64 = true;
+        *started = 1;
     });
 }
 

@@ -103,7 +103,7 @@ void launch_convert(const double *src, int64_t lds, T *dst, int64_t ldd, int n, 
                     cudaStream_t s, int *nonfinite = nullptr);
 template <class T>
 void launch_convert_to_f64(const T *src, int64_t lds, double *dst, int64_t ldd, int n,
-                           cudaStream_t s);
+                           cudaStream_t s, int rows = -1);
 template <class T> void launch_fill(T *dst, int64_t ld, int n, double value, cudaStream_t s, int rows = -1);
 // Y = a*X + b*Y  (elementwise, matcher.py:197)
 template <class T>

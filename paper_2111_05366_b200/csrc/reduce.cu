@@ -126,8 +126,8 @@ __global__ void convert_kernel(const double *src, int64_t lds, T *dst, int64_t l
 }
 
 template <class T>
-__global__ void convert_to_f64_kernel(const T *src, int64_t lds, double *dst, int64_t ldd, int n) {
-    for (int i = blockIdx.x; i < n; i += gridDim.x)
+__global__ void convert_to_f64_kernel(const T *src, int64_t lds, double *dst, int64_t ldd, int n, int rows) {
+    for (int i = blockIdx.x; i < rows; i += gridDim.x)
         for (int j = threadIdx.x; j < n; j += kThreads) dst[(int64_t)i * ldd + j] = (double)src[(int64_t)i * lds + j];
 }
 
@@ -247,8 +247,9 @@ void launch_convert(const double *src, int64_t lds, T *dst, int64_t ldd, int n, 
 }
 
 template <class T>
-void launch_convert_to_f64(const T *src, int64_t lds, double *dst, int64_t ldd, int n, cudaStream_t s) {
-    convert_to_f64_kernel<T><<<std::min(n, 4096), kThreads, 0, s>>>(src, lds, dst, ldd, n); note_launch();
+void launch_convert_to_f64(const T *src, int64_t lds, double *dst, int64_t ldd, int n, cudaStream_t s, int rows) {
+    if (rows < 0) rows = n;
+    convert_to_f64_kernel<T><<<std::max(1, std::min(rows, 4096)), kThreads, 0, s>>>(src, lds, dst, ldd, n, rows); note_launch();
     GOAT_CHECK_LAUNCH();
 }
 
@@ -310,7 +311,7 @@ void launch_neglog(const T *X, int64_t ldx, T *Y, int64_t ldy, int n, int *bad, 
     template void launch_fw_dots<T>(const T *, const T *, const T *, const T *, const T *, int64_t, int, \
                                     double *, double *, cudaStream_t, int);                          \
     template void launch_convert<T>(const double *, int64_t, T *, int64_t, int, double, cudaStream_t, int *); \
-    template void launch_convert_to_f64<T>(const T *, int64_t, double *, int64_t, int, cudaStream_t); \
+    template void launch_convert_to_f64<T>(const T *, int64_t, double *, int64_t, int, cudaStream_t, int); \
     template void launch_fill<T>(T *, int64_t, int, double, cudaStream_t, int);                      \
     template void launch_axpby<T>(double, const T *, double, T *, int64_t, int, cudaStream_t, int);  \
     template void launch_perm_matrix<T>(const int *, T *, int64_t, int, cudaStream_t);               \

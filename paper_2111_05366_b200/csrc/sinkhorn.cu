@@ -1021,6 +1021,7 @@ __device__ __forceinline__ void sk_sweeps(const SkArgs &a, unsigned *bar, const 
                                           unsigned &xi, int k0, int K, double tol, double coef, double gmax,
                                           typename VecT<T>::V (&xres)[R][CH], WideRing *rg) {
     const int blk = blockIdx.x, nblk = gridDim.x;
+    const int nostop_k = a.st->nostop_k;
     unsigned epoch = 0;
     for (int k = k0;; ++k) {
         sk_stamp(a, k, 0);
@@ -1043,7 +1044,7 @@ __device__ __forceinline__ void sk_sweeps(const SkArgs &a, unsigned *bar, const 
         if (blk == 0 && threadIdx.x == 0) a.dslot[(k + 1) & 1] = 0ull;  // next sweep's slot
         int stop = 0, sweeps = 0, conv = 0, slot = 0;
         if (k >= 2) {
-            if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
+            if (drow < tol && k > nostop_k) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
             else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
         }
         if (!stop) {
@@ -2422,7 +2423,7 @@ __global__ void __launch_bounds__(kShardMergeThreads) sk_shard_merge_kernel(SkAr
     for (int r = 0; r < world; ++r) drow = fmax(drow, recv[r * ld1 + n]);
     int stop = 0, sweeps = 0, conv = 0, slot = 0;
     if (k >= 2) {
-        if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
+        if (drow < tol && k > st->nostop_k) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
         else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
     }
     __syncthreads();
@@ -2575,7 +2576,7 @@ __global__ void __launch_bounds__(kThreads) sk_merge_kernel(SkArgs a) {
     }
     if (k >= 2) {
         st->last_dev = drow;  // dev_{k-1}
-        if (drow < tol) {
+        if (drow < tol && k > st->nostop_k) {
             st->done = 1; st->sweeps = k - 1; st->converged = 1; st->slot = (k - 1) & 1; st->dev = drow;
             return;
         }
@@ -2748,7 +2749,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
     const double tol = a.st->tol, coef_d = a.st->coef, gmax_d = a.st->gmax;
     const double ks = SkMath<T>::kScale;
     const T coef = (T)(coef_d * ks), gmax = (T)gmax_d;
-    const int k0 = a.st->k;
+    const int k0 = a.st->k, nostop_k = a.st->nostop_k;
     const T *G = static_cast<const T *>(a.G);
     // tile, g slice (from slot k0+1), barriers
     for (int idx = tid; idx < rows_g * SW; idx += kTileThreads) {
@@ -2902,7 +2903,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) sk_tile_kernel(SkArgs a, unsi
         const double drow = __longlong_as_double((long long)__ldcg(a.dslot + 3 + (k % 3)));
         int stop = 0, sweeps = 0, conv = 0, slot = 0;
         if (k >= 2) {
-            if (drow < tol) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
+            if (drow < tol && k > nostop_k) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
             else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
         }
         if (stop) {

@@ -155,6 +155,17 @@ def solve_lap(M, sense: str = "minimize", *, device=0, precision="fp64") -> LapS
     return LapSolution(assignment=p, objective=float(M[np.arange(n), p].sum()))
 
 
+def relaxed_objective(A, B, L, P, *, device=0, precision="fp64") -> float:
+    """f(P) = sum(A^T P B * P) (+ <L, P>) (matcher.py:170-174) = <G(P), P> / 2 with the
+    gradient formed on the device."""
+    P = np.asarray(P, dtype=np.float64)
+    G = gradient(A, B, P, device=device, precision=precision)
+    val = 0.5 * float((G * P).sum())
+    if L is not None:
+        val += float((np.asarray(L, dtype=np.float64) * P).sum())
+    return val
+
+
 #: largest order accepted by the exhaustive tie enumeration (lap.py:22)
 TIE_SET_MAX_N = 10
 

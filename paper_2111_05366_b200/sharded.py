@@ -172,6 +172,12 @@ class GpuShardBackend:
                                                   ctypes.byref(dev), ctypes.byref(r), ctypes.byref(p)))
         return d.value, s.value, c.value, dev.value, r.value, p.value
 
+    def lot_refine(self, G) -> bool:
+        """fp32: re-open a LOT that stopped at the fp32 deviation floor, in fp64 arithmetic."""
+        started = ctypes.c_int32()
+        _lib.check(self.lib.goat_shard_lot_refine(self.h.ptr, G.data_ptr(), ctypes.byref(started)))
+        return bool(started.value)
+
     def lot_repair_pass(self, G, pairs):
         _lib.check(self.lib.goat_shard_lot_repair_pass(self.h.ptr, G.data_ptr(), pairs.data_ptr()))
 
@@ -249,7 +255,16 @@ def sharded_fw_core(backend, comm: Comm, A_rows, AT_rows, B, *, max_iters=30, ma
         backend.lot_begin(sense_code, lam, lo, hi, max_sweeps, sk_tol)
         done, sweeps, conv, _, _, pending = backend.lot_status()
         rounds = 0
-        while not done:
+        refined = False
+        while True:
+            if done:
+                # fp32 sweeps that stopped at the fp32 deviation floor go on in fp64
+                # (every rank holds the same loop state, so all take the same branch)
+                if refined or not backend.lot_refine(G):
+                    break
+                refined = True
+                done, sweeps, conv, _, _, pending = backend.lot_status()
+                continue
             # `poll` sweeps per host check; once a sweep is left pending for a column
             # repair the rest of the chunk is no-ops on every rank
             for _ in range(poll):

@@ -80,13 +80,23 @@ def lot_log32(E, max_sweeps, tol):
     return Q.numpy(), sw, dev
 
 
-def run(A, B, round_g, round_q, lot32, max_iters=30, fw_tol=1e-2):
+def run(A, B, round_g, round_q, lot32, max_iters=30, fw_tol=1e-2, g_noise=0.0, g_trunc=0, final_exact=False):
     n = A.shape[0]
     At, Bt = torch.from_numpy(A), torch.from_numpy(B)
+    rng = np.random.default_rng(1)
 
-    def grad(P):
+    def grad(P, final=False):
         Pt = torch.from_numpy(P)
         G = (At @ Pt @ Bt.t() + At.t() @ Pt @ Bt).numpy()
+        if final and final_exact:  # the LAP input formed in float64 from the (rounded) iterate
+            return G
+        if g_noise:  # a gradient accurate to g_noise * max|G| (e.g. a split-bf16 tensor-core product)
+            G = G + g_noise * np.abs(G).max() * rng.standard_normal(G.shape)
+        if g_trunc:  # the iterate cut to g_trunc mantissa bits before the product (bf16 planes)
+            m, e = np.frexp(P)
+            Pc = np.ldexp(np.trunc(m * 2.0 ** g_trunc) / 2.0 ** g_trunc, e)
+            Pc = torch.from_numpy(Pc)
+            G = (At @ Pc @ Bt.t() + At.t() @ Pc @ Bt).numpy()
         return G.astype(np.float32).astype(np.float64) if round_g else G
 
     def rel(P):
@@ -114,7 +124,7 @@ def run(A, B, round_g, round_q, lot32, max_iters=30, fw_tol=1e-2):
         print(f"  it {i}: sweeps {sw} dev {dev:.3e} alpha {a} step {step:.4f}", flush=True)
         if step < fw_tol:
             break
-    G = grad(P)
+    G = grad(P, final=True)
     p, _ = O.lap(G, "maximize")
     return p, sweeps, alphas, O.qap_objective_perm(A, B, p)
 
@@ -125,14 +135,18 @@ def main():
     ap.add_argument("--round-g", action="store_true")
     ap.add_argument("--round-q", action="store_true")
     ap.add_argument("--lot32", action="store_true")
+    ap.add_argument("--g-noise", type=float, default=0.0)
+    ap.add_argument("--g-trunc", type=int, default=0)
+    ap.add_argument("--final-exact", action="store_true")
     args = ap.parse_args()
     A, B, _ = graphs.config_pair(args.config, 0)
     z = np.load(os.path.join(ROOT, "tests/golden/full_cases.npz"))
     key = f"c{args.config}_full"
     t0 = time.time()
-    p, sw, al, obj = run(A, B, args.round_g, args.round_q, args.lot32)
+    p, sw, al, obj = run(A, B, args.round_g, args.round_q, args.lot32, g_noise=args.g_noise, g_trunc=args.g_trunc, final_exact=args.final_exact)
     same = np.array_equal(p, z[f"{key}/alignment"])
-    print(f"config {args.config} round_g={args.round_g} round_q={args.round_q} lot32={args.lot32}: "
+    print(f"config {args.config} round_g={args.round_g} round_q={args.round_q} lot32={args.lot32} "
+          f"g_noise={args.g_noise} g_trunc={args.g_trunc} final_exact={args.final_exact}: "
           f"sweeps {sw} (ref {z[f'{key}/lot_sweeps'].tolist()}) alpha {al} obj {obj} "
           f"(ref {float(z[f'{key}/objective'])}) same_perm={same} "
           f"perm_agree={np.mean(p == z[f'{key}/alignment']):.4f} {time.time() - t0:.0f}s", flush=True)

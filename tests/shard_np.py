@@ -135,6 +135,9 @@ class NumpyShardBackend:
     def lot_status(self):
         return self.done, self.sweeps, self.conv, self.dev, self.repaired, self.pending
 
+    def lot_refine(self, G):
+        return False  # float64 arithmetic throughout: nothing to finish
+
     def lot_repair_pass(self, G, pairs):
         if not self.pending:
             return

@@ -34,6 +34,7 @@ def _cost(n):
     d2 = torch.randint(50, 150, (n,), device="cuda", generator=g).float()
     G = torch.zeros((n, ld), device="cuda")
     G[:, :n] = torch.outer(d1, d2) / n + torch.rand((n, n), device="cuda", generator=g)
+    torch.cuda.synchronize()  # the library runs on the handle's own stream, not torch's
     return G
 
 
