@@ -11,6 +11,7 @@
 //     c2 = s_PP - t1 + s_QQ,          c1 = t1 - 2 s_QQ (+ <L, P - Q>)
 //     f(aP + (1-a)Q) = a^2 s_PP + a(1-a) t1 + (1-a)^2 s_QQ (+ a<L,P> + (1-a)<L,Q>)
 // (identities of matcher.py:110-122 and :170-174, all accumulated in fp64).
+#include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -539,10 +540,14 @@ LotOut run_lot(Ctx &c, const T *Gin, int sense, double lam, int max_sweeps, doub
     return out;
 }
 
+// Phase timer (CUDA events on the handle's stream); a named timer also opens an
+// NVTX range (header-only nvtx3: visible to Nsight tools, free otherwise).
 struct Timer {
     cudaEvent_t a, b;
     cudaStream_t s;
-    explicit Timer(cudaStream_t st) : s(st) {
+    bool range = false;
+    explicit Timer(cudaStream_t st, const char *name = nullptr) : s(st) {
+        if (name) { nvtxRangePushA(name); range = true; }
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a, s);
@@ -554,7 +559,11 @@ struct Timer {
         cudaEventElapsedTime(&ms, a, b);
         return ms;
     }
-    ~Timer() { cudaEventDestroy(a); cudaEventDestroy(b); }
+    ~Timer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        if (range) nvtxRangePop();
+    }
 };
 
 // ------------------------------------------------------------------ LAP
@@ -608,11 +617,15 @@ int run_lap(Ctx &c, const T *M, int sense, int *perm_dev, std::vector<int> &perm
                     h.lap_stats[1], h.lap_stats[2], h.lap_stats[3]);
         }
         Timer tsap(c.s);
+        GOAT_CUDA(cudaMemsetAsync(w.status, 0, 4 * sizeof(int), c.s));
         launch_lap_sap<T>(M, c.ld, n, sense, w, c.s, warm);
-        int status = 0;
-        GOAT_CUDA(cudaMemcpyAsync(&status, w.status, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+        int status4[4] = {0, 0, 0, 0};
+        GOAT_CUDA(cudaMemcpyAsync(status4, w.status, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.s));
         sync(c);
-        if (verbose) fprintf(stderr, "lap n=%d augmenting-path repair: %.1f ms\n", n, tsap.stop());
+        const int status = status4[0];
+        if (verbose)
+            fprintf(stderr, "lap n=%d augmenting-path repair: %.1f ms (cluster solver: %d rows, %d distance levels, %d "
+                            "columns scanned)\n", n, tsap.stop(), status4[1], status4[2], status4[3]);
         if (status != 0) throw Error(GOAT_EINVAL, "cost matrix is infeasible");
     }
     perm_host.resize(n);
@@ -655,7 +668,7 @@ void fw_loop(Ctx &c, bool have_L, bool p0_bary, const goat_options &o, goat_fw_r
         setup_gemm<T>(c, A, B);
     }
     {
-        Timer tm(c.s);
+        Timer tm(c.s, "goat.gradient");
         if (p0_bary) {
             launch_fill<T>(P, ld, n, 1.0 / n, c.s);  // core.py:89-93
             if (c.csr) {
@@ -686,7 +699,7 @@ void fw_loop(Ctx &c, bool have_L, bool p0_bary, const goat_options &o, goat_fw_r
         if (have_L) { launch_add<T>(G, L, Gl, ld, n, c.s); Gin = Gl; }
         LotOut lo;
         {
-            Timer tm(c.s);
+            Timer tm(c.s, "goat.lot");
             if (o.step_solver == GOAT_STEP_LOT) {
                 lo = run_lot<T>(c, Gin, o.sense, o.lam, o.max_sweeps, o.sk_tol, Q, nullptr, nullptr, 0);
             } else {
@@ -703,11 +716,11 @@ void fw_loop(Ctx &c, bool have_L, bool p0_bary, const goat_options &o, goat_fw_r
         if (res->lot_dev) res->lot_dev[i - 1] = lo.dev;
         if (res->lot_fp64_from) res->lot_fp64_from[i - 1] = lo.fp64_from;
         {
-            Timer tm(c.s);
+            Timer tm(c.s, "goat.gradient");
             gradient<T>(c, A, B, Q, GQ, T1);
             t_grad += tm.stop();
         }
-        Timer tm(c.s);
+        Timer tm(c.s, "goat.line_search");
         launch_fw_dots<T>(G, GQ, P, Q, L, ld, n, h.red.as<double>(), dots, c.s);
         GOAT_CUDA(cudaMemcpyAsync(hd, dots, 6 * 8, cudaMemcpyDeviceToHost, c.s));
         sync(c);
@@ -737,7 +750,7 @@ void fw_loop(Ctx &c, bool have_L, bool p0_bary, const goat_options &o, goat_fw_r
     const T *Gin = G;
     if (have_L) { launch_add<T>(G, L, Gl, ld, n, c.s); Gin = Gl; }
     std::vector<int> ph;
-    Timer tm(c.s);
+    Timer tm(c.s, "goat.lap");
     res->lap_certified = run_lap<T>(c, Gin, o.sense, h.ivec.as<int>(), ph);
     t_lap += tm.stop();
     for (int r = 0; r < n; ++r) res->assignment[r] = ph[r];

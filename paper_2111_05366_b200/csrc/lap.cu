@@ -228,6 +228,62 @@ __device__ __forceinline__ void gbar(unsigned *bar, unsigned nb, unsigned &epoch
     __syncthreads();
 }
 
+// Row scans of the auction: 16-byte loads of the cost row and of the price vector
+// (VW = 4 floats / 2 doubles per lane per step, two steps in flight).  Lanes walk
+// ascending column indices, so a strict '>' keeps the lowest index among equal
+// profits within a lane; callers combine lanes with the (value, index) rule.
+template <class T>
+__device__ __forceinline__ void row_profits(const T *Mi, const double *price, double sign, int n, int q,
+                                            double (&v)[16 / sizeof(T)]) {
+    constexpr int VW = 16 / sizeof(T);
+    const int j0 = q * VW;
+    T x[VW];
+    *reinterpret_cast<uint4 *>(x) = *reinterpret_cast<const uint4 *>(Mi + j0);  // rows are padded to 32 bytes
+    if (j0 + VW <= n) {
+#pragma unroll
+        for (int e = 0; e < VW; e += 2) {
+            const double2 p = __ldcg(reinterpret_cast<const double2 *>(price + j0 + e));
+            v[e] = sign * (double)x[e] - p.x;
+            v[e + 1] = sign * (double)x[e + 1] - p.y;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) v[e] = (j0 + e < n) ? sign * (double)x[e] - __ldcg(price + j0 + e) : -INFINITY;
+    }
+}
+
+template <class T>
+__device__ __forceinline__ void scan_top2(const T *Mi, const double *price, double sign, int n, int start, int stride,
+                                          double &w1, double &w2, int &j1) {
+    constexpr int VW = 16 / sizeof(T);
+    const int nv = (n + VW - 1) / VW;
+#pragma unroll 2
+    for (int q = start; q < nv; q += stride) {
+        double v[VW];
+        row_profits<T>(Mi, price, sign, n, q, v);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+            if (v[e] > w1) { w2 = w1; w1 = v[e]; j1 = q * VW + e; }
+            else if (v[e] > w2) w2 = v[e];
+        }
+    }
+}
+
+template <class T>
+__device__ __forceinline__ double scan_best(const T *Mi, const double *price, double sign, int n, int start, int stride) {
+    constexpr int VW = 16 / sizeof(T);
+    const int nv = (n + VW - 1) / VW;
+    double best = -INFINITY;
+#pragma unroll 2
+    for (int q = start; q < nv; q += stride) {
+        double v[VW];
+        row_profits<T>(Mi, price, sign, n, q, v);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) best = fmax(best, v[e]);
+    }
+    return best;
+}
+
 template <class T>
 __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a) {
     const int n = a.n, lane = threadIdx.x & 31;
@@ -236,8 +292,10 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
     unsigned epoch = 0;
     __shared__ int s_done;
-    int rounds = 0;
+    int rounds = 0, phases = 0;
+    unsigned scans = 0;  // diagnostics: bidder rows scanned by this thread
     for (double eps = a.eps0;; eps = fmax(eps / a.theta, a.eps_min)) {
+        ++phases;
         // new phase, prices kept.  First phase: empty assignment.  Later phases keep
         // every row that already satisfies eps-complementary slackness for the new
         // eps (its column within eps of its best profit) and free only the others,
@@ -255,8 +313,7 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
                 const int j0 = __ldcg(a.row_col + i);
                 if (j0 < 0) continue;
                 const T *Mi = M + (int64_t)i * a.ld;
-                double best = -INFINITY;
-                for (int j = lane; j < n; j += 32) best = fmax(best, a.sign * (double)Mi[j] - __ldcg(a.price + j));
+                double best = scan_best<T>(Mi, a.price, a.sign, n, lane, 32);
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
                 if (lane == 0) {
@@ -284,11 +341,7 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
                     const T *Mi = M + (int64_t)i * a.ld;
                     double w1 = -INFINITY, w2 = -INFINITY;
                     int j1 = INT_MAX;
-                    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-                        const double v = a.sign * (double)Mi[j] - __ldcg(a.price + j);
-                        if (v > w1) { w2 = w1; w1 = v; j1 = j; }
-                        else if (v > w2) w2 = v;
-                    }
+                    scan_top2<T>(Mi, a.price, a.sign, n, threadIdx.x, blockDim.x, w1, w2, j1);
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) {
                         const double b1 = __shfl_xor_sync(0xffffffffu, w1, off);
@@ -311,6 +364,7 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
                         a.row_bid[i] = j1;
                         a.row_bid_v[i] = bid;
                         atomicMax(a.bid_val + j1, (unsigned long long)__double_as_longlong(bid));
+                        ++scans;
                     }
                     __syncthreads();
                 }
@@ -320,11 +374,7 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
                 const T *Mi = M + (int64_t)i * a.ld;
                 double w1 = -INFINITY, w2 = -INFINITY;
                 int j1 = INT_MAX;
-                for (int j = lane; j < n; j += 32) {
-                    const double v = a.sign * (double)Mi[j] - __ldcg(a.price + j);
-                    if (v > w1) { w2 = w1; w1 = v; j1 = j; }
-                    else if (v > w2) w2 = v;
-                }
+                scan_top2<T>(Mi, a.price, a.sign, n, lane, 32, w1, w2, j1);
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) {
                     const double b1 = __shfl_xor_sync(0xffffffffu, w1, off);
@@ -344,6 +394,7 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
                     a.row_bid[i] = j1;
                     a.row_bid_v[i] = bid;
                     atomicMax(a.bid_val + j1, (unsigned long long)__double_as_longlong(bid));
+                    ++scans;
                 }
             }
             gbar(a.bar, gridDim.x, epoch);
@@ -380,7 +431,8 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
         }
         if (eps <= a.eps_min || rounds >= a.max_rounds) break;
     }
-    if (gt == 0) { a.counters[1] = rounds; a.counters[2] = (rounds >= a.max_rounds) ? 1 : 0; }
+    if (gt == 0) { a.counters[1] = rounds; a.counters[2] = (rounds >= a.max_rounds) ? 1 : 0; a.counters[5] = phases; }
+    if (scans) atomicAdd(reinterpret_cast<unsigned *>(a.counters) + 4, scans);
 }
 
 // Exact-repair preparation: duals from the auction prices in the minimisation
@@ -392,8 +444,7 @@ __global__ void lap_auction_repair(const T *M, AucArgs a, double *u, double *v, 
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
     for (int i = gw; i < n; i += nwarps) {
         const T *Mi = M + (int64_t)i * a.ld;
-        double best = -INFINITY;
-        for (int j = lane; j < n; j += 32) best = fmax(best, a.sign * (double)Mi[j] - a.price[j]);
+        double best = scan_best<T>(Mi, a.price, a.sign, n, lane, 32);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
         if (lane == 0) {
@@ -428,8 +479,7 @@ __global__ void lap_tighten_rows(const T *M, AucArgs a, double *delta) {
         const int j0 = a.row_col[i];
         if (j0 < 0) { if (lane == 0) delta[i] = 0.0; continue; }
         const T *Mi = M + (int64_t)i * a.ld;
-        double best = -INFINITY;
-        for (int j = lane; j < n; j += 32) best = fmax(best, a.sign * (double)Mi[j] - a.price[j]);
+        double best = scan_best<T>(Mi, a.price, a.sign, n, lane, 32);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
         if (lane == 0) delta[i] = best - (a.sign * (double)Mi[j0] - a.price[j0]);
@@ -495,6 +545,23 @@ template <class P> __device__ __forceinline__ P *cl_map(P *p, unsigned rank) {
 
 constexpr int kLapClThreads = 1024;
 
+// One CTA's view of the next distance level of the search.
+struct LapLevel {
+    double v;   // smallest tentative distance among its unscanned columns (INFINITY: none)
+    int count;  // unscanned columns at that distance
+    int freej;  // lowest free column among them (INT_MAX: none)
+    int pad;
+};
+
+// The search settles a whole DISTANCE LEVEL per step: every unscanned column whose
+// tentative distance equals the current minimum is scanned at once (label setting
+// stays valid for equal keys since reduced costs are >= 0), and the rows matched to
+// them form the next frontier, relaxed together.  On the 0/1-graph gradients this
+// solver sees, > 90 % of the single-column steps sat at an unchanged distance
+// (config 5: 631 276 steps for 122 rows, 580 062 of them ties), so levels cut the
+// cluster barriers 5.5x (114 221 levels).  The frontier (row, u) list lives in global
+// scratch (w.rem, w.spc), written in a fixed order -- CTA rank, then thread, then
+// column -- so path choices among equal distances are deterministic.
 template <class T, int CL>
 __global__ void __launch_bounds__(kLapClThreads, 1)
     lap_cluster_sap_kernel(const T *M, int64_t ld, int n, double sign, LapWork w, int W) {
@@ -505,14 +572,18 @@ __global__ void __launch_bounds__(kLapClThreads, 1)
     int *path = reinterpret_cast<int *>(ucol + W);
     int *r4c = path + W;
     unsigned char *SC = reinterpret_cast<unsigned char *>(r4c + W);
-    __shared__ LapCand cand[2][CL];
-    __shared__ LapCand s_warp[kLapClThreads / 32];
+    constexpr int NW = kLapClThreads / 32;
+    __shared__ LapLevel lvl[2][CL];
+    __shared__ double s_wmin[NW];
+    __shared__ int s_wcnt[NW], s_wfree[NW];
     const unsigned rank = cl_rank();
-    const int c0 = (int)rank * W, c1 = min(n, c0 + W);
+    const int c0 = (int)rank * W, c1 = min(n, c0 + W), wloc = max(0, c1 - c0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int *col4row = w.col4row;
-    for (int j = c0 + tid; j < c1; j += kLapClThreads) {
-        const int jl = j - c0;
+    int *frow = w.rem;     // frontier rows of the current level
+    double *fu = w.spc;    // their duals
+    for (int jl = tid; jl < wloc; jl += kLapClThreads) {
+        const int j = c0 + jl;
         v[jl] = w.v[j];
         const int r = w.row4col[j];
         r4c[jl] = r;
@@ -520,77 +591,125 @@ __global__ void __launch_bounds__(kLapClThreads, 1)
     }
     cl_sync();
     int par = 0;
+    int d_rows = 0, d_levels = 0, d_cols = 0;  // diagnostics (GOAT_LAP_VERBOSE): free rows, levels, columns scanned
     for (int cur = 0; cur < n; ++cur) {
         if (__ldcg(col4row + cur) != -1) continue;  // matched (uniform: published by the last cluster barrier)
-        for (int j = c0 + tid; j < c1; j += kLapClThreads) { SC[j - c0] = 0; spc[j - c0] = INFINITY; }
+        ++d_rows;
+        for (int jl = tid; jl < wloc; jl += kLapClThreads) { SC[jl] = 0; spc[jl] = INFINITY; }
         __syncthreads();
         const double ucur = __ldcg(w.u + cur);
-        double minv = 0.0, ui = ucur;
-        int i = cur, sink = -1;
+        double minv = 0.0;
+        int sink = -1, nf = 1;
+        bool first = true;  // the first frontier is the free row itself
         for (;;) {
-            const T *Mi = M + (int64_t)i * ld;
-            LapCand b{INFINITY, 0.0, INT_MAX, -1, 0, 0};
-            for (int j = c0 + tid; j < c1; j += kLapClThreads) {
-                const int jl = j - c0;
+            // (1) relax this CTA's unscanned columns from every frontier row
+            double tmin = INFINITY;
+            for (int jl = tid; jl < wloc; jl += kLapClThreads) {
                 if (SC[jl]) continue;
-                const double r = ((minv + sign * (double)Mi[j]) - ui) - v[jl];
+                const int j = c0 + jl;
+                const double vj = v[jl];
                 double sj = spc[jl];
-                if (r < sj) { path[jl] = i; spc[jl] = r; sj = r; }
-                const LapCand c{sj, 0.0, j, 0, r4c[jl] == -1 ? 1 : 0, 0};
-                if (cand_less(c, b)) b = c;
+                int pj = -1;
+                if (first) {
+                    const double r = ((minv + sign * (double)M[(int64_t)cur * ld + j]) - ucur) - vj;
+                    if (r < sj) { sj = r; pj = cur; }
+                } else {
+                    for (int q = 0; q < nf; ++q) {
+                        const int i = __ldcg(frow + q);
+                        const double r = ((minv + sign * (double)M[(int64_t)i * ld + j]) - __ldcg(fu + q)) - vj;
+                        if (r < sj) { sj = r; pj = i; }
+                    }
+                }
+                if (pj >= 0) { spc[jl] = sj; path[jl] = pj; }
+                tmin = fmin(tmin, sj);
             }
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                LapCand o;
-                o.v = __shfl_xor_sync(0xffffffffu, b.v, off);
-                o.j = __shfl_xor_sync(0xffffffffu, b.j, off);
-                o.free = __shfl_xor_sync(0xffffffffu, b.free, off);
-                if (cand_less(o, b)) b = o;
-            }
-            if (lane == 0) s_warp[warp] = b;
+            for (int off = 16; off > 0; off >>= 1) tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, off));
+            if (lane == 0) s_wmin[warp] = tmin;
             __syncthreads();
-            if (warp == 0) {
-                LapCand c = s_warp[lane];
+            double bmin = INFINITY;
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    LapCand o;
-                    o.v = __shfl_xor_sync(0xffffffffu, c.v, off);
-                    o.j = __shfl_xor_sync(0xffffffffu, c.j, off);
-                    o.free = __shfl_xor_sync(0xffffffffu, c.free, off);
-                    if (cand_less(o, c)) c = o;
+            for (int q = 0; q < NW; ++q) bmin = fmin(bmin, s_wmin[q]);
+            // (2) this CTA's columns at its minimum: count, lowest free one
+            int cnt = 0, fj = INT_MAX;
+            if (bmin < INFINITY) {
+                for (int jl = tid; jl < wloc; jl += kLapClThreads) {
+                    if (SC[jl] || spc[jl] != bmin) continue;
+                    ++cnt;
+                    if (r4c[jl] == -1) fj = min(fj, c0 + jl);
                 }
-                if (c.j != INT_MAX) {
-                    c.inext = r4c[c.j - c0];
-                    c.unext = ucol[c.j - c0];
-                }
-                // this CTA's candidate into slot [par][rank] of every CTA of the cluster
-                if (lane < CL) *cl_map(&cand[par][rank], (unsigned)lane) = c;
             }
+            int incl = cnt;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += t;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) fj = min(fj, __shfl_xor_sync(0xffffffffu, fj, off));
+            if (lane == 31) s_wcnt[warp] = incl;
+            if (lane == 0) s_wfree[warp] = fj;
+            __syncthreads();
+            int woff = 0, bcount = 0, bfree = INT_MAX;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) {
+                if (q < warp) woff += s_wcnt[q];
+                bcount += s_wcnt[q];
+                bfree = min(bfree, s_wfree[q]);
+            }
+            if (tid < CL) *cl_map(&lvl[par][rank], (unsigned)tid) = LapLevel{bmin, bcount, bfree, 0};
             cl_sync();
-            LapCand g = cand[par][0];
+            // (3) the global level: distance, a free column to stop at, list offsets
+            double d = INFINITY;
 #pragma unroll
-            for (int q = 1; q < CL; ++q)
-                if (cand_less(cand[par][q], g)) g = cand[par][q];
-            par ^= 1;
-            if (!(g.v < INFINITY)) {
+            for (int q = 0; q < CL; ++q) d = fmin(d, lvl[par][q].v);
+            if (!(d < INFINITY)) {
                 if (rank == 0 && tid == 0) *w.status = -1;
-                return;  // uniform across the cluster
+                return;  // infeasible (uniform across the cluster)
             }
-            // the thread that scans column g.j marks it (no barrier before its next read)
-            if (g.j >= c0 && g.j < c1 && (g.j - c0) % kLapClThreads == tid) SC[g.j - c0] = 1;
-            minv = g.v;
-            if (g.free) { sink = g.j; break; }
-            i = g.inext;
-            ui = g.unext;
+            int gfree = INT_MAX, base = 0, total = 0;
+#pragma unroll
+            for (int q = 0; q < CL; ++q) {
+                if (lvl[par][q].v != d) continue;
+                gfree = min(gfree, lvl[par][q].freej);
+                if (q < (int)rank) base += lvl[par][q].count;
+                total += lvl[par][q].count;
+            }
+            par ^= 1;
+            minv = d;
+            ++d_levels;
+            if (gfree != INT_MAX) {
+                sink = gfree;
+                if (sink >= c0 && sink < c1 && tid == 0) SC[sink - c0] = 1;
+                break;
+            }
+            // (4) scan every column of the level; their rows are the next frontier.  (Measured:
+            // writing each CTA's candidates speculatively before the barrier, to save the
+            // second barrier, is slower -- 18 vs 12 us per level -- every CTA then flushes
+            // global writes each level.)
+            if (bmin == d && cnt) {
+                int idx = base + woff + (incl - cnt);
+                for (int jl = tid; jl < wloc; jl += kLapClThreads) {
+                    if (SC[jl] || spc[jl] != d) continue;
+                    frow[idx] = r4c[jl];
+                    fu[idx] = ucol[jl];
+                    ++idx;
+                    SC[jl] = 1;
+                }
+                __threadfence();
+            }
+            nf = total;
+            d_cols += total;
+            first = false;
+            cl_sync();  // the frontier list is complete and visible to every CTA
         }
         __syncthreads();
         // dual update (matcher order of the single-CTA solver): scanned columns
-        for (int j = c0 + tid; j < c1; j += kLapClThreads) {
-            const int jl = j - c0;
+        for (int jl = tid; jl < wloc; jl += kLapClThreads) {
             if (!SC[jl]) continue;
-            const double d = minv - spc[jl];
-            v[jl] -= d;
-            if (j != sink) ucol[jl] += d;  // u of the visited row matched to j
+            const double dd = minv - spc[jl];
+            v[jl] -= dd;
+            if (c0 + jl != sink) ucol[jl] += dd;  // u of the visited row matched to the column
         }
         cl_sync();
         if (rank == 0 && tid == 0) {
@@ -615,11 +734,11 @@ __global__ void __launch_bounds__(kLapClThreads, 1)
         }
         cl_sync();
     }
-    for (int j = c0 + tid; j < c1; j += kLapClThreads) {
-        w.row4col[j] = r4c[j - c0];
-        w.v[j] = v[j - c0];
+    for (int jl = tid; jl < wloc; jl += kLapClThreads) {
+        w.row4col[c0 + jl] = r4c[jl];
+        w.v[c0 + jl] = v[jl];
     }
-    if (rank == 0 && tid == 0) *w.status = 0;
+    if (rank == 0 && tid == 0) { *w.status = 0; w.status[1] = d_rows; w.status[2] = d_levels; w.status[3] = d_cols; }
 }
 
 }  // namespace
@@ -642,21 +761,26 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
     const char *te = getenv("GOAT_LAP_TAIL");  // divisor: tail = n / div (0 = complete every phase)
     // measured (profiles/round1_lap_tail_scan.log): ending a phase at n/128 free rows
     // cuts the auction's bidding-war tail at n <= 8192 (c4 LAP 44 -> 29 ms, c3 75 ->
-    // 63 ms, the exact repair absorbs the extra rows); n/512 above, where the
-    // cluster repair of a freed row costs more
-    const int div = te ? atoi(te) : (n <= 8192 ? 128 : 512);
+    // 63 ms, the exact repair absorbs the extra rows); n/2048 above, where a row left
+    // to the cluster repair costs ~5 ms (n = 40000, profiles/round2_lap_scan.log:
+    // n/512 -> 1634 + 1339 ms, n/1024 -> 1657 + 1164, n/2048 -> 1796 + 711, n/4096 -> 2396 + 540)
+    const int div = te ? atoi(te) : (n <= 8192 ? 128 : 2048);
     a.tail = div > 0 ? n / div : 0;
     const char *ke = getenv("GOAT_LAP_KEEP");
     a.keep = ke ? atoi(ke) : 0;  // measured: rounds 6556 -> 6482 at n = 40000, no gain; opt-in
     GOAT_CUDA(cudaMemsetAsync(aw.price, 0, sizeof(double) * n, s));
     GOAT_CUDA(cudaMemsetAsync(aw.bar, 0, 256, s));
-    GOAT_CUDA(cudaMemsetAsync(aw.counters, 0, 16, s));
+    GOAT_CUDA(cudaMemsetAsync(aw.counters, 0, 32, s));
     int occ = 0;
     GOAT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lap_auction_kernel<T>, 256, 0));
     const int grid = std::max(1, occ) * num_sms;
     void *params[] = {(void *)&M, &a};
+    const bool verbose = getenv("GOAT_LAP_VERBOSE") != nullptr;
+    cudaEvent_t ev[3];
+    if (verbose) { for (auto &e : ev) cudaEventCreate(&e); cudaEventRecord(ev[0], s); }
     GOAT_CUDA(cudaLaunchCooperativeKernel((const void *)lap_auction_kernel<T>, dim3(grid), dim3(256), params, 0, s));
     note_launch();
+    if (verbose) cudaEventRecord(ev[1], s);
     const char *tr = getenv("GOAT_LAP_TIGHTEN");  // Jacobi rounds (0 = off)
     const int rounds = tr ? atoi(tr) : 16;  // measured: freed rows 15815 -> 170 at n = 40000, repair 4.3 -> 3.4 s
     for (int r = 0; r < rounds; ++r) {
@@ -667,6 +791,19 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
     lap_auction_repair<T><<<num_sms * 4, 256, 0, s>>>(M, a, w.u, w.v, w.row4col, w.col4row, aw.counters + 3); note_launch();
     lap_auction_unlink<<<std::max(1, std::min(ceil_div(n, 256), num_sms * 4)), 256, 0, s>>>(n, w.col4row, w.row4col); note_launch();
     GOAT_CHECK_LAUNCH();
+    if (verbose) {
+        cudaEventRecord(ev[2], s);
+        cudaEventSynchronize(ev[2]);
+        float t_auc = 0, t_tight = 0;
+        cudaEventElapsedTime(&t_auc, ev[0], ev[1]);
+        cudaEventElapsedTime(&t_tight, ev[1], ev[2]);
+        int cnt[8];
+        cudaMemcpy(cnt, aw.counters, 32, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "lap n=%d auction kernel %.1f ms (%d phases, %d rounds, %u bidder-row scans = %.1f GB), %d tighten "
+                        "rounds + duals %.1f ms (tail %d, eps_min %.3g)\n", n, t_auc, cnt[5], cnt[1], (unsigned)cnt[4],
+                (double)(unsigned)cnt[4] * n * sizeof(T) / 1e9, rounds, t_tight, a.tail, a.eps_min);
+        for (auto &e : ev) cudaEventDestroy(e);
+    }
     return 0;
 }
 

@@ -7,10 +7,13 @@ returned objective (integer-exact for c3's 0/1 graphs), the iteration count,
 the convergence flag, the alpha sequence and every LOT's sweep count must equal
 the reference's (matcher.py:177-212, core.py:120-124).
 
-fp32 mode: see DESIGN.md §4 for the measured fp32 floor.  c4 reproduces the
-reference; c3's final LAP is hub-dominated (match ratio 0.002 against the
-planted permutation) and separates optimal assignments by less than fp32
-rounding of the gradient, so fp32 is checked against the bound stated there.
+fp32 mode: every LOT finishes in fp64 arithmetic below the fp32
+deviation floor, so the per-LOT sweep counts follow the reference's.  c4
+reproduces the reference's permutation.  c3 fails recovery (match ratio 0.002);
+its last iteration is an endpoint tie (f(P) = f(Q) to 11 digits, alpha in {0, 1})
+and its final LAP moves under a 3e-8 relative perturbation of the gradients even
+inside the reference (profiles/round2_precision_study.txt), so fp32 is held to the
+trajectory (sweeps and alphas up to the tie) and a 1e-3 objective bound.
 """
 import hashlib
 
@@ -62,3 +65,17 @@ def test_full_c4_fp32_matches_reference():
     np.testing.assert_array_equal(res.alignment, FULL[f"{key}/alignment"])
     assert res.objective == pytest.approx(float(FULL[f"{key}/objective"]), rel=1e-6)
     assert res.iterations == int(FULL[f"{key}/iterations"])
+
+
+def test_full_c3_fp32_follows_reference_trajectory():
+    A, B, key = _inputs(3)
+    res = gb.frank_wolfe_match(A, B, gb.MatchOptions(step_solver="lot", precision="fp32"))
+    ref_sweeps = FULL[f"{key}/lot_sweeps"].tolist()
+    ref_alpha = FULL[f"{key}/hist_alpha"][1:]
+    k = len(ref_sweeps) - 1  # everything before the terminal endpoint tie
+    assert res.diagnostics["lot_sweeps"][:k] == ref_sweeps[:k]
+    np.testing.assert_allclose(_alphas(res)[1:k + 1], ref_alpha[:k], atol=1e-6)
+    np.testing.assert_allclose([h[1] for h in res.iterate_history[:k + 1]], FULL[f"{key}/hist_obj"][:k + 1], rtol=1e-5)
+    assert res.iterations in (len(ref_sweeps), len(ref_sweeps) + 1)
+    assert res.objective == pytest.approx(float(FULL[f"{key}/objective"]), rel=1e-3)
+    assert sorted(res.alignment.tolist()) == list(range(A.shape[0]))
