@@ -337,3 +337,17 @@ def test_nonfinite_inputs_raise_valueerror(which, bad):
     (A if which == "A" else B)[3, 7] = bad
     with pytest.raises(ValueError, match=f"{which} contains non-finite entries"):
         gb.frank_wolfe_match(A, B, gb.MatchOptions(step_solver="lot"))
+
+
+def test_bit_identical_reruns_at_c2():
+    """Identical inputs and options give a bit-identical MatchResult including the
+    iterate history (test_matcher.py:160-170), at config 2's size and in both
+    precisions (fixed reduction trees, no order-varying atomics on the value path)."""
+    case = "c2_r0"
+    for precision in ("fp64", "fp32"):
+        a, b = _run(case, precision), _run(case, precision)
+        np.testing.assert_array_equal(a.alignment, b.alignment)
+        assert a.objective == b.objective and a.iterations == b.iterations
+        assert a.iterate_history == b.iterate_history
+        assert a.diagnostics["lot_sweeps"] == b.diagnostics["lot_sweeps"]
+        assert a.diagnostics["lot_deviation"] == b.diagnostics["lot_deviation"]
