@@ -208,6 +208,7 @@ struct AucArgs {
     double *row_bid_v;     // [n]
     unsigned *bar;         // grid barrier counter (zeroed)
     int *counters;         // [0] assigned columns, [1] rounds (diagnostic), [2] status
+    int *list;             // [n] unassigned rows of the round (built when they outnumber the CTAs)
     int max_rounds;
     int tail;              // a phase ends once at most `tail` rows are unassigned
     int keep;              // later phases keep the rows that satisfy eps-CS
@@ -266,6 +267,67 @@ __device__ __forceinline__ void scan_top2(const T *Mi, const double *price, doub
             if (v[e] > w1) { w2 = w1; w1 = v[e]; j1 = q * VW + e; }
             else if (v[e] > w2) w2 = v[e];
         }
+    }
+}
+
+// R rows per warp: the price vector is loaded once per column step and shared by the
+// R row loads (the price reads are 2/3 of the L2->SM traffic of a one-row scan).
+template <class T, int R>
+__device__ __forceinline__ void scan_top2_rows(const T *const (&Mi)[R], const double *price, double sign, int n,
+                                               int start, int stride, double (&w1)[R], double (&w2)[R], int (&j1)[R]) {
+    constexpr int VW = 16 / sizeof(T);
+    const int nv = (n + VW - 1) / VW;
+    for (int q = start; q < nv; q += stride) {
+        const int j0 = q * VW;
+        double p[VW];
+        if (j0 + VW <= n) {
+#pragma unroll
+            for (int e = 0; e < VW; e += 2) {
+                const double2 pp = __ldcg(reinterpret_cast<const double2 *>(price + j0 + e));
+                p[e] = pp.x;
+                p[e + 1] = pp.y;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < VW; ++e) p[e] = (j0 + e < n) ? __ldcg(price + j0 + e) : INFINITY;  // profit -inf
+        }
+        T x[R][VW];
+#pragma unroll
+        for (int k = 0; k < R; ++k) *reinterpret_cast<uint4 *>(x[k]) = *reinterpret_cast<const uint4 *>(Mi[k] + j0);
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                const double v = sign * (double)x[k][e] - p[e];
+                if (v > w1[k]) { w2[k] = w1[k]; w1[k] = v; j1[k] = j0 + e; }
+                else if (v > w2[k]) w2[k] = v;
+            }
+    }
+}
+
+// Named barrier of a warp group inside a CTA (ids 1-4 as immediates, so the kernel
+// reserves 5 barriers instead of all 16).
+__device__ __forceinline__ void group_bar(int grp, int threads) {
+    switch (grp) {
+        case 0: asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory"); break;
+        case 1: asm volatile("bar.sync 2, %0;" ::"r"(threads) : "memory"); break;
+        case 2: asm volatile("bar.sync 3, %0;" ::"r"(threads) : "memory"); break;
+        default: asm volatile("bar.sync 4, %0;" ::"r"(threads) : "memory"); break;
+    }
+}
+
+// (best, second, lowest index of the best) of two partial scans
+__device__ __forceinline__ void top2_merge(double &w1, double &w2, int &j1, double b1, double b2, int bj) {
+    if (b1 > w1 || (b1 == w1 && bj < j1)) { w2 = fmax(b2, w1); w1 = b1; j1 = bj; }
+    else w2 = fmax(w2, b1);
+}
+__device__ __forceinline__ void top2_warp(double &w1, double &w2, int &j1) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double b1 = __shfl_xor_sync(0xffffffffu, w1, off);
+        const double b2 = __shfl_xor_sync(0xffffffffu, w2, off);
+        const int bj = __shfl_xor_sync(0xffffffffu, j1, off);
+        top2_merge(w1, w2, j1, b1, b2, bj);
     }
 }
 
@@ -329,72 +391,116 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
         for (int j = gt; j < n; j += nt) { a.bid_val[j] = 0ull; a.bid_row[j] = INT_MAX; a.row_bid[j] = -1; }
         gbar(a.bar, gridDim.x, epoch);
         for (;;) {
-            // (A) bids of unassigned rows.  Few bidders (late rounds of a phase): a
-            // whole CTA scans each bidder's row (8x the warps on the row scan);
-            // otherwise a warp per bidder.  Same (best, second, lowest-index) result.
+            // (A) bids of unassigned rows: (best, second best, lowest index of the best) of
+            // val_ij - p_j over the row, whatever the work split.  The split follows the
+            // number of bidders so every round streams rows at full width: at most one
+            // bidder per CTA -> a CTA per row; more -> the bidders are compacted into a
+            // list and taken by groups of 4 / 2 warps, a warp per row, or 2 / 4 rows per
+            // warp (one load of the price vector serves the rows of a warp).
+            auto post_bid = [&](int i, double w1, double w2, int j1) {
+                const double gap = (w2 == -INFINITY) ? 0.0 : (w1 - w2);
+                const double bid = __ldcg(a.price + j1) + gap + eps;
+                a.row_bid[i] = j1;
+                a.row_bid_v[i] = bid;
+                atomicMax(a.bid_val + j1, (unsigned long long)__double_as_longlong(bid));
+                ++scans;
+            };
+            __shared__ double s_w1[8], s_w2[8];
+            __shared__ int s_j1[8];
+            const int wib = threadIdx.x >> 5;
             if (n - __ldcg(a.counters) <= (int)gridDim.x) {
-                __shared__ double s_w1[8], s_w2[8];
-                __shared__ int s_j1[8];
-                const int wib = threadIdx.x >> 5;
                 for (int i = blockIdx.x; i < n; i += gridDim.x) {
                     if (__ldcg(a.row_col + i) != -1) continue;  // uniform in the CTA
                     const T *Mi = M + (int64_t)i * a.ld;
                     double w1 = -INFINITY, w2 = -INFINITY;
                     int j1 = INT_MAX;
                     scan_top2<T>(Mi, a.price, a.sign, n, threadIdx.x, blockDim.x, w1, w2, j1);
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) {
-                        const double b1 = __shfl_xor_sync(0xffffffffu, w1, off);
-                        const double b2 = __shfl_xor_sync(0xffffffffu, w2, off);
-                        const int bj = __shfl_xor_sync(0xffffffffu, j1, off);
-                        if (b1 > w1 || (b1 == w1 && bj < j1)) { w2 = fmax(b2, w1); w1 = b1; j1 = bj; }
-                        else w2 = fmax(w2, b1);
-                    }
+                    top2_warp(w1, w2, j1);
                     if (lane == 0) { s_w1[wib] = w1; s_w2[wib] = w2; s_j1[wib] = j1; }
                     __syncthreads();
                     if (threadIdx.x == 0) {
-                        for (int q = 1; q < (int)(blockDim.x >> 5); ++q) {
-                            const double b1 = s_w1[q], b2 = s_w2[q];
-                            const int bj = s_j1[q];
-                            if (b1 > w1 || (b1 == w1 && bj < j1)) { w2 = fmax(b2, w1); w1 = b1; j1 = bj; }
-                            else w2 = fmax(w2, b1);
-                        }
-                        const double gap = (w2 == -INFINITY) ? 0.0 : (w1 - w2);
-                        const double bid = __ldcg(a.price + j1) + gap + eps;
-                        a.row_bid[i] = j1;
-                        a.row_bid_v[i] = bid;
-                        atomicMax(a.bid_val + j1, (unsigned long long)__double_as_longlong(bid));
-                        ++scans;
+                        for (int q = 1; q < (int)(blockDim.x >> 5); ++q) top2_merge(w1, w2, j1, s_w1[q], s_w2[q], s_j1[q]);
+                        post_bid(i, w1, w2, j1);
                     }
                     __syncthreads();
                 }
-            } else
-            for (int i = gw; i < n; i += nwarps) {
-                if (__ldcg(a.row_col + i) != -1) continue;
-                const T *Mi = M + (int64_t)i * a.ld;
-                double w1 = -INFINITY, w2 = -INFINITY;
-                int j1 = INT_MAX;
-                scan_top2<T>(Mi, a.price, a.sign, n, lane, 32, w1, w2, j1);
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    const double b1 = __shfl_xor_sync(0xffffffffu, w1, off);
-                    const double b2 = __shfl_xor_sync(0xffffffffu, w2, off);
-                    const int bj = __shfl_xor_sync(0xffffffffu, j1, off);
-                    if (b1 > w1 || (b1 == w1 && bj < j1)) {
-                        w2 = fmax(b2, w1);
-                        w1 = b1;
-                        j1 = bj;
-                    } else {
-                        w2 = fmax(w2, b1);
+            } else {
+                // compact the bidders (the list order varies between runs; each row's bid
+                // does not depend on it)
+                for (int i = gt; i < n; i += nt)
+                    if (__ldcg(a.row_col + i) == -1) a.list[atomicAdd(a.counters + 6, 1)] = i;
+                gbar(a.bar, gridDim.x, epoch);
+                const int nb = __ldcg(a.counters + 6);
+                if (nb * 2 <= nwarps) {
+                    // GW warps of a CTA per row
+                    const int GW = (nb * 4 <= nwarps) ? 4 : 2;
+                    const int gpc = 8 / GW, grp = wib / GW, tig = threadIdx.x - grp * GW * 32;
+                    for (int idx = blockIdx.x * gpc + grp; idx < nb; idx += (int)gridDim.x * gpc) {
+                        const int i = __ldcg(a.list + idx);
+                        const T *Mi = M + (int64_t)i * a.ld;
+                        double w1 = -INFINITY, w2 = -INFINITY;
+                        int j1 = INT_MAX;
+                        scan_top2<T>(Mi, a.price, a.sign, n, tig, GW * 32, w1, w2, j1);
+                        top2_warp(w1, w2, j1);
+                        if (lane == 0) { s_w1[wib] = w1; s_w2[wib] = w2; s_j1[wib] = j1; }
+                        group_bar(grp, GW * 32);
+                        if (tig == 0) {
+                            for (int q = 1; q < GW; ++q) top2_merge(w1, w2, j1, s_w1[wib + q], s_w2[wib + q], s_j1[wib + q]);
+                            post_bid(i, w1, w2, j1);
+                        }
+                        group_bar(grp, GW * 32);
                     }
-                }
-                if (lane == 0) {
-                    const double gap = (w2 == -INFINITY) ? 0.0 : (w1 - w2);
-                    const double bid = __ldcg(a.price + j1) + gap + eps;
-                    a.row_bid[i] = j1;
-                    a.row_bid_v[i] = bid;
-                    atomicMax(a.bid_val + j1, (unsigned long long)__double_as_longlong(bid));
-                    ++scans;
+                } else if (nb < nwarps + nwarps / 2) {
+                    for (int idx = gw; idx < nb; idx += nwarps) {
+                        const int i = __ldcg(a.list + idx);
+                        double w1 = -INFINITY, w2 = -INFINITY;
+                        int j1 = INT_MAX;
+                        scan_top2<T>(M + (int64_t)i * a.ld, a.price, a.sign, n, lane, 32, w1, w2, j1);
+                        top2_warp(w1, w2, j1);
+                        if (lane == 0) post_bid(i, w1, w2, j1);
+                    }
+                } else if (nb < 3 * nwarps) {
+                    constexpr int R = 2;
+                    for (int base = gw * R; base < nb; base += nwarps * R) {
+                        int rows[R];
+                        const T *Mi[R];
+                        double w1[R], w2[R];
+                        int j1[R];
+#pragma unroll
+                        for (int k = 0; k < R; ++k) {
+                            rows[k] = __ldcg(a.list + min(base + k, nb - 1));
+                            Mi[k] = M + (int64_t)rows[k] * a.ld;
+                            w1[k] = w2[k] = -INFINITY;
+                            j1[k] = INT_MAX;
+                        }
+                        scan_top2_rows<T, R>(Mi, a.price, a.sign, n, lane, 32, w1, w2, j1);
+#pragma unroll
+                        for (int k = 0; k < R; ++k) {
+                            top2_warp(w1[k], w2[k], j1[k]);
+                            if (lane == 0 && base + k < nb) post_bid(rows[k], w1[k], w2[k], j1[k]);
+                        }
+                    }
+                } else {
+                    constexpr int R = 4;
+                    for (int base = gw * R; base < nb; base += nwarps * R) {
+                        int rows[R];
+                        const T *Mi[R];
+                        double w1[R], w2[R];
+                        int j1[R];
+#pragma unroll
+                        for (int k = 0; k < R; ++k) {
+                            rows[k] = __ldcg(a.list + min(base + k, nb - 1));
+                            Mi[k] = M + (int64_t)rows[k] * a.ld;
+                            w1[k] = w2[k] = -INFINITY;
+                            j1[k] = INT_MAX;
+                        }
+                        scan_top2_rows<T, R>(Mi, a.price, a.sign, n, lane, 32, w1, w2, j1);
+#pragma unroll
+                        for (int k = 0; k < R; ++k) {
+                            top2_warp(w1[k], w2[k], j1[k]);
+                            if (lane == 0 && base + k < nb) post_bid(rows[k], w1[k], w2[k], j1[k]);
+                        }
+                    }
                 }
             }
             gbar(a.bar, gridDim.x, epoch);
@@ -420,6 +526,7 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
                 a.bid_row[j] = INT_MAX;
             }
             for (int i = gt; i < n; i += nt) a.row_bid[i] = -1;
+            if (gt == 0) a.counters[6] = 0;  // next round's bidder list
             gbar(a.bar, gridDim.x, epoch);
             ++rounds;
             // The last few bidders of a phase fight long price wars on near-tied
@@ -758,13 +865,17 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
     a.price = aw.price; a.row_col = aw.row_col; a.col_row = aw.col_row; a.bid_val = aw.bid_val;
     a.bid_row = aw.bid_row; a.row_bid = aw.row_bid; a.row_bid_v = aw.row_bid_v; a.bar = aw.bar;
     a.counters = aw.counters; a.max_rounds = 200000;
+    a.list = w.rem;  // free until the repair
     const char *te = getenv("GOAT_LAP_TAIL");  // divisor: tail = n / div (0 = complete every phase)
     // measured (profiles/round1_lap_tail_scan.log): ending a phase at n/128 free rows
     // cuts the auction's bidding-war tail at n <= 8192 (c4 LAP 44 -> 29 ms, c3 75 ->
-    // 63 ms, the exact repair absorbs the extra rows); n/2048 above, where a row left
+    // 63 ms, the exact repair absorbs the extra rows); n/2048 beyond it, where a row left
     // to the cluster repair costs ~5 ms (n = 40000, profiles/round2_lap_scan.log:
     // n/512 -> 1634 + 1339 ms, n/1024 -> 1657 + 1164, n/2048 -> 1796 + 711, n/4096 -> 2396 + 540)
-    const int div = te ? atoi(te) : (n <= 8192 ? 128 : 2048);
+    // (the switch follows the repair solver: one CTA while its state fits shared memory,
+    // the same test launch_lap_sap makes, else the cluster solver)
+    const bool one_cta_repair = (size_t)n * (8 + 8 + 4 + 4 + 4 + 1) + 16 <= 200 * 1024;
+    const int div = te ? atoi(te) : (one_cta_repair ? 128 : 2048);
     a.tail = div > 0 ? n / div : 0;
     const char *ke = getenv("GOAT_LAP_KEEP");
     a.keep = ke ? atoi(ke) : 0;  // measured: rounds 6556 -> 6482 at n = 40000, no gain; opt-in

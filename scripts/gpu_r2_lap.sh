@@ -1,7 +1,7 @@
 #!/bin/bash
 # c5 final LAP: auction / tighten / repair split under the tail knob
 cd $GRAFT_REPO_ROOT
-for cfg in "GOAT_LAP_TAIL=512" "GOAT_LAP_TAIL=1024" "GOAT_LAP_TAIL=2048" "GOAT_LAP_TAIL=4096"; do
+for cfg in "GOAT_LAP_TAIL=2048" "GOAT_LAP_TAIL=1024" "GOAT_LAP_TAIL=4096" "GOAT_LAP_TAIL=8192"; do
   echo "== $cfg"
   env $cfg GOAT_LAP_VERBOSE=1 timeout 600 python scripts/run_c5.py 5 40000 fp32 csr 2>&1 | grep -v "^$" | cut -c1-700 | tail -6
 done
