@@ -212,6 +212,7 @@ struct AucArgs {
     int max_rounds;
     int tail;              // a phase ends once at most `tail` rows are unassigned
     int keep;              // later phases keep the rows that satisfy eps-CS
+    int stall;             // a phase also ends after `stall` rounds without a new minimum of unassigned rows (0 = never)
 };
 
 __device__ __forceinline__ unsigned ld_acq(const unsigned *p) {
@@ -390,6 +391,7 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
         }
         for (int j = gt; j < n; j += nt) { a.bid_val[j] = 0ull; a.bid_row[j] = INT_MAX; a.row_bid[j] = -1; }
         gbar(a.bar, gridDim.x, epoch);
+        int best_un = INT_MAX, since = 0;  // thread 0 of every CTA tracks the same counters: uniform
         for (;;) {
             // (A) bids of unassigned rows: (best, second best, lowest index of the best) of
             // val_ij - p_j over the row, whatever the work split.  The split follows the
@@ -532,7 +534,14 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
             // The last few bidders of a phase fight long price wars on near-tied
             // columns; the exact repair assigns them far cheaper, so a phase stops
             // at `tail` unassigned rows (the next phase restarts from the prices).
-            if (threadIdx.x == 0) s_done = (__ldcg(a.counters) >= n - a.tail) || rounds >= a.max_rounds;
+            // Exact ties (0/1-graph gradients, integer costs) make the last bidders trade a
+            // column back and forth in eps-sized steps: a phase that has not reached a new
+            // minimum of unassigned rows for `stall` rounds hands them to the repair too.
+            if (threadIdx.x == 0) {
+                const int un = n - __ldcg(a.counters);
+                if (un < best_un) { best_un = un; since = 0; } else ++since;
+                s_done = un <= a.tail || rounds >= a.max_rounds || (a.stall > 0 && since >= a.stall);
+            }
             __syncthreads();
             if (s_done) break;
         }
@@ -877,6 +886,8 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
     const bool one_cta_repair = (size_t)n * (8 + 8 + 4 + 4 + 4 + 1) + 16 <= 200 * 1024;
     const int div = te ? atoi(te) : (one_cta_repair ? 128 : 2048);
     a.tail = div > 0 ? n / div : 0;
+    const char *se = getenv("GOAT_LAP_STALL");
+    a.stall = se ? atoi(se) : 0;
     const char *ke = getenv("GOAT_LAP_KEEP");
     a.keep = ke ? atoi(ke) : 0;  // measured: rounds 6556 -> 6482 at n = 40000, no gain; opt-in
     GOAT_CUDA(cudaMemsetAsync(aw.price, 0, sizeof(double) * n, s));

@@ -53,3 +53,27 @@ def test_cluster_repair_matches_scipy(n, kind, sense, monkeypatch):
     gb.as_permutation(sol.assignment)
     if not np.array_equal(sol.assignment, p):
         assert M[np.arange(n), sol.assignment].sum() == M[np.arange(n), p].sum()
+
+
+@pytest.mark.parametrize("kind", ["uniform", "tied"])
+def test_large_order_bidder_list_paths(kind):
+    """n = 7500: beyond the single-CTA repair (cluster solver by default) and with more
+    bidders than warps in the first rounds of a phase, so the auction's bidder-list
+    splits (1, 2 and 4 rows per warp) and the level-wise cluster repair all run.
+    `uniform` is checked against scipy.  `tied` is a rank-1 product of small integer
+    degree vectors -- exact ties everywhere, the shape of FAQ's first gradient; scipy
+    needs minutes on it, but its optimum is known in closed form (rearrangement
+    inequality: sort both vectors)."""
+    n = 7500
+    rng = np.random.default_rng(75 + (kind == "tied"))
+    if kind == "uniform":
+        M = rng.random((n, n)).astype(np.float32).astype(np.float64)
+        v = O.lap(M, "maximize")[1]
+    else:
+        d1 = rng.integers(1, 21, n).astype(np.float64)
+        d2 = rng.integers(1, 21, n).astype(np.float64)
+        M = np.outer(d1, d2)
+        v = float(np.dot(np.sort(d1), np.sort(d2)))
+    sol = gb.solve_lap(M, "maximize", precision="fp32")
+    gb.as_permutation(sol.assignment)
+    assert sol.objective == v
