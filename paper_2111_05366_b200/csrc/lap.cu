@@ -985,6 +985,18 @@ void launch_lap_sap(const T *M, int64_t ld, int n, int sense, const LapWork &w, 
             return;
         }
     }
+    // warm repair that fits one CTA: GOAT_LAP_LEVELS=1 runs the level-wise solver on a
+    // cluster of one instead of the single-column solver below.  Off by default: without
+    // exact ties a level is one column and costs two barriers more (c3 final LAP, n = 5000:
+    // 35.6 vs 19.6 ms; c4, n = 2000: 27.0 vs 27.3 ms -- profiles/round2_lap_levels_one_cta.log).
+    const char *lve = getenv("GOAT_LAP_LEVELS");
+    if (warm && lve && atoi(lve) == 1) {
+        const double sign1 = (sense == GOAT_MAXIMIZE) ? -1.0 : 1.0;
+        if (try_cluster_sap<T, 1>(M, ld, n, sign1, w, s)) {
+            GOAT_CHECK_LAUNCH();
+            return;
+        }
+    }
     int use_smem = smem <= 200 * 1024;
     if (use_smem)
         GOAT_CUDA(cudaFuncSetAttribute(lap_sap_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -121,3 +121,18 @@ def test_sharded_csr_c5_n4000_matches_golden():
     np.testing.assert_array_equal(r.assignment, g["assignment"])
     np.testing.assert_allclose(r.hist_alpha[1:], g["alpha"], atol=1e-6)
     assert r.lot_sweeps == g["sweeps"].tolist()
+
+
+def test_sharded_csr_c5_n4000_fp32_matches_golden():
+    """The same run in fp32 mode: the sharded LOT finishes in fp64 arithmetic below the
+    fp32 deviation floor exactly like the single-GPU path (goat_shard_lot_refine), so
+    the row-sharded fp32 solve returns the oracle's permutation and objective too, with
+    per-LOT sweep counts within one of the oracle's."""
+    from paper_2111_05366_b200 import graphs
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c5_n4000.npz"))
+    A, Bs, truth = graphs.config_pair(5, 0, n=4000)
+    r = sharded_match(A, Bs, precision="fp32", max_iters=4)
+    assert r.iterations == int(g["iterations"]) and r.converged == bool(g["converged"])
+    np.testing.assert_array_equal(r.assignment, g["assignment"])
+    np.testing.assert_allclose(r.hist_alpha[1:], g["alpha"], atol=1e-5)
+    assert max(abs(a - b) for a, b in zip(r.lot_sweeps, g["sweeps"].tolist())) <= 1
