@@ -624,26 +624,11 @@ __global__ void lap_auction_unlink(int n, const int *col4row, int *row4col) {
 // outgrows shared memory, so every Dijkstra step streams ~25 bytes per column
 // through one SM.  Here CL CTAs split the columns into contiguous slices held in
 // shared memory (spc, v, path, row4col, and ucol = u of the row matched to the
-// column), each step reads only its slice of the cost row, and the step's argmin
-// is a candidate exchange through distributed shared memory plus one cluster
-// barrier.  Ties: smallest reduced cost, then a free column, then the lowest
-// index (deterministic).  Dual updates and the augmentation are the same as the
-// single-CTA solver, so the result is an exact optimum (scipy's, up to ties).
-struct LapCand {
-    double v;      // reduced cost
-    double unext;  // u of the row matched to column j
-    int j;         // column (INT_MAX: none)
-    int inext;     // row matched to j (-1: free)
-    int free;
-    int pad;
-};
-
-__device__ __forceinline__ bool cand_less(const LapCand &a, const LapCand &b) {
-    if (a.v != b.v) return a.v < b.v;
-    if (a.free != b.free) return a.free > b.free;
-    return a.j < b.j;
-}
-
+// column); a step reads only each CTA's slice of the frontier rows, and its minimum
+// is an exchange through distributed shared memory plus cluster barriers.  Ties:
+// smallest reduced cost, then a free column (the lowest index).  Dual updates and
+// the augmentation are those of the single-CTA solver, so the result is an exact
+// optimum (scipy's value; on ties possibly another optimal permutation).
 __device__ __forceinline__ unsigned cl_rank() {
     unsigned r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
