@@ -11,4 +11,5 @@ timeout 600 python scripts/fp32_status.py fp32 > gpurun_out/r2g_fp32.jsonl 2> gp
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r2g_bench_ref.json 2> gpurun_out/r2g_bench_ref.err; echo "ref rc=$?"
 timeout 1500 python bench.py --steps 3 --warmup 3 > gpurun_out/r2g_bench.json 2> gpurun_out/r2g_bench.err; echo "bench rc=$?"
 GOAT_BENCH_SECONDARY=0 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r2g_launches.csv python bench.py --steps 1 --warmup 3 > gpurun_out/r2g_ncu_bench.log 2>&1; echo "ncu list rc=$?"
+GOAT_BENCH_SHARDED=1 timeout 1500 python bench.py --steps 1 --warmup 3 > gpurun_out/r2g_bench_sharded_w1.json 2> gpurun_out/r2g_bench_sharded_w1.err; echo "sharded world-1 rc=$?"
 cut -c1-1400 gpurun_out/r2g_bench.json
