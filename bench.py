@@ -474,6 +474,7 @@ def run_sharded(args):
 
     rank, world, local = _dist()
     torch.cuda.set_device(local)
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # NCCL's version / debug lines stay off stdout (one JSON line)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
     os.environ.setdefault("RANK", "0")
