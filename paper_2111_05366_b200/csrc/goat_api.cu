@@ -598,7 +598,7 @@ int run_lap(Ctx &c, const T *M, int sense, int *perm_dev, std::vector<int> &perm
             for (int q = 0; q < 2; ++q) h.auc_d[q].ensure(vb);
             for (int q = 0; q < 4; ++q) h.auc_i[q].ensure(ib);
             h.auc_u64.ensure(vb);
-            h.auc_misc.ensure(512);
+            h.auc_misc.ensure(512 + (size_t)kAucMaxCtas * 24);
             AuctionWork aw{};
             aw.price = h.auc_d[0].as<double>(); aw.row_bid_v = h.auc_d[1].as<double>();
             aw.row_col = h.auc_i[0].as<int>(); aw.col_row = h.auc_i[1].as<int>();
@@ -606,6 +606,8 @@ int run_lap(Ctx &c, const T *M, int sense, int *perm_dev, std::vector<int> &perm
             aw.bid_val = h.auc_u64.as<unsigned long long>();
             aw.counters = h.auc_misc.as<int>();
             aw.bar = reinterpret_cast<unsigned *>(h.auc_misc.as<char>() + 256);
+            aw.part_w = reinterpret_cast<double *>(h.auc_misc.as<char>() + 512);
+            aw.part_j = reinterpret_cast<int *>(h.auc_misc.as<char>() + 512 + (size_t)kAucMaxCtas * 16);
             launch_lap_auction<T>(M, c.ld, n, sense, lohi[1] - lohi[0], w, aw, h.num_sms, c.s);
             GOAT_CUDA(cudaMemcpyAsync(h.lap_stats, aw.counters, 16, cudaMemcpyDeviceToHost, c.s));
             warm = 1;

@@ -183,7 +183,10 @@ struct AuctionWork {
     int *row_col, *col_row, *bid_row, *row_bid, *counters;
     unsigned long long *bid_val;
     unsigned *bar;
+    double *part_w;  // [2 * kAucMaxCtas] per-CTA partial (best, second) of a shared row scan
+    int *part_j;     // [kAucMaxCtas]
 };
+constexpr int kAucMaxCtas = 4096;
 template <class T>
 int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, const LapWork &w,
                        const AuctionWork &aw, int num_sms, cudaStream_t s);

@@ -208,7 +208,9 @@ struct AucArgs {
     double *row_bid_v;     // [n]
     unsigned *bar;         // grid barrier counter (zeroed)
     int *counters;         // [0] assigned columns, [1] rounds (diagnostic), [2] status
-    int *list;             // [n] unassigned rows of the round (built when they outnumber the CTAs)
+    int *list;             // [n] unassigned rows of the round
+    double *part_w;        // [2 * CTAs] (best, second) of a CTA's share of a row (few-bidder rounds)
+    int *part_j;           // [CTAs] its best column
     int max_rounds;
     int tail;              // a phase ends once at most `tail` rows are unassigned
     int keep;              // later phases keep the rows that satisfy eps-CS
@@ -348,7 +350,7 @@ __device__ __forceinline__ double scan_best(const T *Mi, const double *price, do
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a) {
+__global__ void __launch_bounds__(256, 3) lap_auction_kernel(const T *M, AucArgs a) {
     const int n = a.n, lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -410,21 +412,46 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
             __shared__ double s_w1[8], s_w2[8];
             __shared__ int s_j1[8];
             const int wib = threadIdx.x >> 5;
-            if (n - __ldcg(a.counters) <= (int)gridDim.x) {
-                for (int i = blockIdx.x; i < n; i += gridDim.x) {
-                    if (__ldcg(a.row_col + i) != -1) continue;  // uniform in the CTA
+            // diagnostics (GOAT_LAP_VERBOSE): rounds and time of phase (A) per work split
+            unsigned long long t_a0 = 0;
+            int regime = 0;
+            if (gt == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_a0));
+            if (n - __ldcg(a.counters) <= (int)gridDim.x / 2) {
+                // few bidders (the long tail of a phase: 6820 of config 5's 8082 rounds):
+                // P = CTAs / bidders CTAs share each row, column-interleaved, and meet
+                // through a per-CTA partial in global scratch (one extra grid barrier) --
+                // a lone CTA streaming a 160 KB row took 86 us per round.
+                for (int i = gt; i < n; i += nt)
+                    if (__ldcg(a.row_col + i) == -1) a.list[atomicAdd(a.counters + 6, 1)] = i;
+                gbar(a.bar, gridDim.x, epoch);
+                const int nb = __ldcg(a.counters + 6);
+                const int P = max(1, min(16, (int)gridDim.x / max(nb, 1)));
+                const int idx = blockIdx.x / P, part = blockIdx.x - idx * P;
+                if (idx < nb) {
+                    const int i = __ldcg(a.list + idx);
                     const T *Mi = M + (int64_t)i * a.ld;
                     double w1 = -INFINITY, w2 = -INFINITY;
                     int j1 = INT_MAX;
-                    scan_top2<T>(Mi, a.price, a.sign, n, threadIdx.x, blockDim.x, w1, w2, j1);
+                    scan_top2<T>(Mi, a.price, a.sign, n, part * (int)blockDim.x + threadIdx.x, P * (int)blockDim.x, w1, w2, j1);
                     top2_warp(w1, w2, j1);
                     if (lane == 0) { s_w1[wib] = w1; s_w2[wib] = w2; s_j1[wib] = j1; }
                     __syncthreads();
                     if (threadIdx.x == 0) {
                         for (int q = 1; q < (int)(blockDim.x >> 5); ++q) top2_merge(w1, w2, j1, s_w1[q], s_w2[q], s_j1[q]);
-                        post_bid(i, w1, w2, j1);
+                        a.part_w[2 * blockIdx.x] = w1;
+                        a.part_w[2 * blockIdx.x + 1] = w2;
+                        a.part_j[blockIdx.x] = j1;
                     }
-                    __syncthreads();
+                }
+                gbar(a.bar, gridDim.x, epoch);
+                if (idx < nb && part == 0 && threadIdx.x == 0) {
+                    double w1 = -INFINITY, w2 = -INFINITY;
+                    int j1 = INT_MAX;
+                    for (int q = 0; q < P; ++q) {  // fixed order: deterministic
+                        const int b = blockIdx.x + q;
+                        top2_merge(w1, w2, j1, __ldcg(a.part_w + 2 * b), __ldcg(a.part_w + 2 * b + 1), __ldcg(a.part_j + b));
+                    }
+                    post_bid(__ldcg(a.list + idx), w1, w2, j1);
                 }
             } else {
                 // compact the bidders (the list order varies between runs; each row's bid
@@ -433,6 +460,7 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
                     if (__ldcg(a.row_col + i) == -1) a.list[atomicAdd(a.counters + 6, 1)] = i;
                 gbar(a.bar, gridDim.x, epoch);
                 const int nb = __ldcg(a.counters + 6);
+                regime = nb * 4 <= nwarps ? 1 : nb * 2 <= nwarps ? 2 : nb < nwarps + nwarps / 2 ? 3 : nb < 3 * nwarps ? 4 : 5;
                 if (nb * 2 <= nwarps) {
                     // GW warps of a CTA per row
                     const int GW = (nb * 4 <= nwarps) ? 4 : 2;
@@ -483,8 +511,16 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
                         }
                     }
                 } else {
-                    constexpr int R = 4;
-                    for (int base = gw * R; base < nb; base += nwarps * R) {
+                    // most of the scan volume (config 5: 617 rounds, ~25 000 bidders each):
+                    // 4 rows per warp, and the CTA walks the columns in tiles whose prices
+                    // are staged once in shared memory for its 32 row scans (the fp64 price
+                    // reads were 2/3 of a row scan's L2->SM traffic, 1/3 with 4 rows per warp)
+                    constexpr int R = 4, TC = 2048, VW = 16 / sizeof(T);
+                    __shared__ __align__(16) double s_price[2][TC];
+                    const int passes = ((nb + R - 1) / R + nwarps - 1) / nwarps;  // uniform over the grid
+                    for (int ps = 0; ps < passes; ++ps) {
+                        const int base = (ps * nwarps + gw) * R;
+                        const bool active = base < nb;
                         int rows[R];
                         const T *Mi[R];
                         double w1[R], w2[R];
@@ -496,16 +532,54 @@ __global__ void __launch_bounds__(256) lap_auction_kernel(const T *M, AucArgs a)
                             w1[k] = w2[k] = -INFINITY;
                             j1[k] = INT_MAX;
                         }
-                        scan_top2_rows<T, R>(Mi, a.price, a.sign, n, lane, 32, w1, w2, j1);
+                        for (int t0 = 0, buf = 0; t0 < n; t0 += TC, buf ^= 1) {
+                            // the other buffer was last read two tiles ago: every warp has passed
+                            // the barrier of the previous tile since
+                            for (int c = threadIdx.x; c < TC; c += blockDim.x)
+                                s_price[buf][c] = (t0 + c < n) ? __ldcg(a.price + t0 + c) : INFINITY;  // profit -inf
+                            __syncthreads();
+                            if (!active) continue;
+#pragma unroll 2
+                            for (int q = lane; q < TC / VW; q += 32) {
+                                const int j0 = t0 + q * VW;
+                                if (j0 >= n) break;
+                                double p[VW];
+#pragma unroll
+                                for (int e = 0; e < VW; e += 2) {
+                                    const double2 pp = *reinterpret_cast<const double2 *>(&s_price[buf][q * VW + e]);
+                                    p[e] = pp.x;
+                                    p[e + 1] = pp.y;
+                                }
+                                T x[R][VW];
+#pragma unroll
+                                for (int k = 0; k < R; ++k)
+                                    *reinterpret_cast<uint4 *>(x[k]) = *reinterpret_cast<const uint4 *>(Mi[k] + j0);
+#pragma unroll
+                                for (int k = 0; k < R; ++k)
+#pragma unroll
+                                    for (int e = 0; e < VW; ++e) {
+                                        const double v = a.sign * (double)x[k][e] - p[e];
+                                        if (v > w1[k]) { w2[k] = w1[k]; w1[k] = v; j1[k] = j0 + e; }
+                                        else if (v > w2[k]) w2[k] = v;
+                                    }
+                            }
+                        }
 #pragma unroll
                         for (int k = 0; k < R; ++k) {
                             top2_warp(w1[k], w2[k], j1[k]);
                             if (lane == 0 && base + k < nb) post_bid(rows[k], w1[k], w2[k], j1[k]);
                         }
+                        __syncthreads();  // the price buffers are rewritten by the next pass
                     }
                 }
             }
             gbar(a.bar, gridDim.x, epoch);
+            if (gt == 0) {
+                unsigned long long t_a1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_a1));
+                a.counters[8 + regime] += 1;
+                reinterpret_cast<unsigned long long *>(a.counters + 16)[regime] += t_a1 - t_a0;
+            }
             // (B) ties on the winning bid go to the lowest row
             for (int i = gt; i < n; i += nt) {
                 const int j = __ldcg(a.row_bid + i);
@@ -860,6 +934,8 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
     a.bid_row = aw.bid_row; a.row_bid = aw.row_bid; a.row_bid_v = aw.row_bid_v; a.bar = aw.bar;
     a.counters = aw.counters; a.max_rounds = 200000;
     a.list = w.rem;  // free until the repair
+    a.part_w = aw.part_w;
+    a.part_j = aw.part_j;
     const char *te = getenv("GOAT_LAP_TAIL");  // divisor: tail = n / div (0 = complete every phase)
     // measured (profiles/round1_lap_tail_scan.log): ending a phase at n/128 free rows
     // cuts the auction's bidding-war tail at n <= 8192 (c4 LAP 44 -> 29 ms, c3 75 ->
@@ -877,10 +953,10 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
     a.keep = ke ? atoi(ke) : 0;  // measured: rounds 6556 -> 6482 at n = 40000, no gain; opt-in
     GOAT_CUDA(cudaMemsetAsync(aw.price, 0, sizeof(double) * n, s));
     GOAT_CUDA(cudaMemsetAsync(aw.bar, 0, 256, s));
-    GOAT_CUDA(cudaMemsetAsync(aw.counters, 0, 32, s));
+    GOAT_CUDA(cudaMemsetAsync(aw.counters, 0, 128, s));
     int occ = 0;
     GOAT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lap_auction_kernel<T>, 256, 0));
-    const int grid = std::max(1, occ) * num_sms;
+    const int grid = std::min(kAucMaxCtas, std::max(1, occ) * num_sms);
     void *params[] = {(void *)&M, &a};
     const bool verbose = getenv("GOAT_LAP_VERBOSE") != nullptr;
     cudaEvent_t ev[3];
@@ -904,8 +980,12 @@ int launch_lap_auction(const T *M, int64_t ld, int n, int sense, double range, c
         float t_auc = 0, t_tight = 0;
         cudaEventElapsedTime(&t_auc, ev[0], ev[1]);
         cudaEventElapsedTime(&t_tight, ev[1], ev[2]);
-        int cnt[8];
-        cudaMemcpy(cnt, aw.counters, 32, cudaMemcpyDeviceToHost);
+        int cnt[32];
+        cudaMemcpy(cnt, aw.counters, 128, cudaMemcpyDeviceToHost);
+        const unsigned long long *tns = reinterpret_cast<const unsigned long long *>(cnt + 16);
+        const char *names[6] = {"cta/row", "4 warps/row", "2 warps/row", "warp/row", "2 rows/warp", "4 rows/warp"};
+        for (int r = 0; r < 6; ++r)
+            if (cnt[8 + r]) fprintf(stderr, "lap   bidding by %-12s %6d rounds %8.1f ms\n", names[r], cnt[8 + r], tns[r] * 1e-6);
         fprintf(stderr, "lap n=%d auction kernel %.1f ms (%d phases, %d rounds, %u bidder-row scans = %.1f GB), %d tighten "
                         "rounds + duals %.1f ms (tail %d, eps_min %.3g)\n", n, t_auc, cnt[5], cnt[1], (unsigned)cnt[4],
                 (double)(unsigned)cnt[4] * n * sizeof(T) / 1e9, rounds, t_tight, a.tail, a.eps_min);
