@@ -861,7 +861,9 @@ __global__ void __launch_bounds__(kLapClThreads, 1)
             // (4) scan every column of the level; their rows are the next frontier.  (Measured:
             // writing each CTA's candidates speculatively before the barrier, to save the
             // second barrier, is slower -- 18 vs 12 us per level -- every CTA then flushes
-            // global writes each level.)
+            // global writes each level; carrying up to two (row, u) entries per CTA inline in
+            // the level exchange and skipping the list and its barrier for such levels is
+            // slower too, 882 vs 734 ms on config 5's repair.)
             if (bmin == d && cnt) {
                 int idx = base + woff + (incl - cnt);
                 for (int jl = tid; jl < wloc; jl += kLapClThreads) {
