@@ -1,7 +1,9 @@
 #!/bin/bash
-# table-based fp64 exp: fp64 parity + per-sweep times
+# fp64 sweep at n = 40000 / 20000: planner knobs
 cd $GRAFT_REPO_ROOT
-timeout 1200 python -m pytest tests/test_parity_gpu.py tests/test_full_configs_gpu.py tests/test_lot_large_gpu.py tests/test_sharded_gpu.py tests/test_configs_gpu.py -q -p no:cacheprovider > gpurun_out/r2m_tests.log 2>&1
-tail -5 gpurun_out/r2m_tests.log
-for n in 100 1000 5000 20000 40000; do python scripts/prof_sweep.py $n fp64 20; done
-python scripts/run_c5.py 5 40000 fp32 csr 2>&1 | tail -1 | cut -c1-400
+for cfg in "GOAT_SK_VERBOSE=1" "GOAT_SK_TMA=0" "GOAT_SK_STAGES=3" "GOAT_SK_STAGES=4" "GOAT_SK_STAGES=6" "GOAT_SK_MAXCH=4" "GOAT_SK_MAXCH=6" "GOAT_SK_RES=0"; do
+  echo "== $cfg"; env $cfg python scripts/prof_sweep.py 40000 fp64 6 2>&1 | tail -2
+done
+for cfg in "GOAT_SK_VERBOSE=1" "GOAT_SK_TMA=0" "GOAT_SK_MAXCH=4"; do
+  echo "== n=20000 $cfg"; env $cfg python scripts/prof_sweep.py 20000 fp64 10 2>&1 | tail -1
+done
