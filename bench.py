@@ -222,9 +222,9 @@ def _kernel_scan(lib, h, dev, hbm_peak):
     from paper_2111_05366_b200 import _lib
     out = {}
     tf_peak, tf_kind = _bf16_peak()
-    for n in (1000, 2000, 5000, 12288):
+    for n in (1000, 2000, 5000, 12288, 25000, 32768):
         G = torch.rand((n, n), dtype=torch.float32, device=dev) * 100.0
-        ms = _ms_per_sweep(lib, h, n, G, reps=200)
+        ms = _ms_per_sweep(lib, h, n, G, reps=200 if n <= 12288 else 50)
         gbs = n * n * 4 / (ms * 1e-3) / 1e9
         out[f"sinkhorn_sweep_n{n}"] = {"us": ms * 1e3, "GB_s": gbs, "frac_hbm": gbs / hbm_peak,
                                        "bytes": n * n * 4}
