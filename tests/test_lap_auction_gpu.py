@@ -77,3 +77,18 @@ def test_large_order_bidder_list_paths(kind):
     sol = gb.solve_lap(M, "maximize", precision="fp32")
     gb.as_permutation(sol.assignment)
     assert sol.objective == v
+
+
+def test_order_12000_four_rows_per_warp_path_matches_scipy():
+    """n = 12000: the first rounds of every auction phase have more than three bidders
+    per warp, so the 4-rows-per-warp split with shared-memory price tiles runs (the
+    only other order that reaches it in the suite is config 5, which has no scipy
+    reference).  Both handle precisions on the same fp32-representable matrix."""
+    n = 12000
+    rng = np.random.default_rng(120)
+    M = rng.random((n, n)).astype(np.float32).astype(np.float64)
+    v = O.lap(M, "maximize")[1]
+    for precision in ("fp32", "fp64"):
+        sol = gb.solve_lap(M, "maximize", precision=precision)
+        gb.as_permutation(sol.assignment)
+        assert sol.objective == v, precision
