@@ -1047,7 +1047,12 @@ void launch_lap_sap(const T *M, int64_t ld, int n, int sense, const LapWork &w, 
     if (warm && lc != 0 && (smem > 200 * 1024 || lc == 2)) {
         // warm repair too large for one CTA's shared memory: the cluster solver
         const double sign = (sense == GOAT_MAXIMIZE) ? -1.0 : 1.0;
-        if (try_cluster_sap<T, 16>(M, ld, n, sign, w, s) || try_cluster_sap<T, 8>(M, ld, n, sign, w, s)) {
+        // GOAT_LAP_CL=8 prefers the 8-CTA cluster (measurement: config 5's repair 951 vs 734 ms
+        // with 16 CTAs -- twice the columns per thread, each a dependent load per frontier row)
+        const char *cle = getenv("GOAT_LAP_CL");
+        const bool prefer8 = cle && atoi(cle) == 8;
+        if ((prefer8 && try_cluster_sap<T, 8>(M, ld, n, sign, w, s)) || try_cluster_sap<T, 16>(M, ld, n, sign, w, s) ||
+            try_cluster_sap<T, 8>(M, ld, n, sign, w, s)) {
             GOAT_CHECK_LAUNCH();
             return;
         }
