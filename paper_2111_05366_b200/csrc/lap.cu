@@ -777,26 +777,46 @@ __global__ void __launch_bounds__(kLapClThreads, 1)
         int sink = -1, nf = 1;
         bool first = true;  // the first frontier is the free row itself
         for (;;) {
-            // (1) relax this CTA's unscanned columns from every frontier row
+            // (1) relax this CTA's unscanned columns from every frontier row.  A thread's
+            // columns (up to 4 at a time) are relaxed together, frontier rows outermost, so
+            // the cost loads of one row -- cold HBM reads, the longest link of a level --
+            // are independent and overlap: config 5's repair 734 -> 592 ms.  (A column-outer
+            // loop paid one load latency per column: the 8-CTA cluster, with twice the
+            // columns per thread, measured 951 ms.  Batching four frontier rows as well,
+            // 16 loads in flight, measured slower: 862 ms.)
             double tmin = INFINITY;
-            for (int jl = tid; jl < wloc; jl += kLapClThreads) {
-                if (SC[jl]) continue;
-                const int j = c0 + jl;
-                const double vj = v[jl];
-                double sj = spc[jl];
-                int pj = -1;
-                if (first) {
-                    const double r = ((minv + sign * (double)M[(int64_t)cur * ld + j]) - ucur) - vj;
-                    if (r < sj) { sj = r; pj = cur; }
-                } else {
-                    for (int q = 0; q < nf; ++q) {
-                        const int i = __ldcg(frow + q);
-                        const double r = ((minv + sign * (double)M[(int64_t)i * ld + j]) - __ldcg(fu + q)) - vj;
-                        if (r < sj) { sj = r; pj = i; }
+            for (int jb = tid; jb < wloc; jb += 4 * kLapClThreads) {
+                int jl[4];
+                bool act[4];
+                double vj[4], sj[4];
+                int pj[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    jl[c] = jb + c * kLapClThreads;
+                    act[c] = jl[c] < wloc && !SC[jl[c]];
+                    vj[c] = act[c] ? v[jl[c]] : 0.0;
+                    sj[c] = act[c] ? spc[jl[c]] : INFINITY;
+                    pj[c] = -1;
+                }
+                for (int q = 0; q < nf; ++q) {
+                    const int i = first ? cur : __ldcg(frow + q);
+                    const double ui = first ? ucur : __ldcg(fu + q);
+                    const T *Mi = M + (int64_t)i * ld + c0;
+                    T m[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) m[c] = act[c] ? Mi[jl[c]] : T(0);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const double r = ((minv + sign * (double)m[c]) - ui) - vj[c];
+                        if (act[c] && r < sj[c]) { sj[c] = r; pj[c] = i; }
                     }
                 }
-                if (pj >= 0) { spc[jl] = sj; path[jl] = pj; }
-                tmin = fmin(tmin, sj);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (!act[c]) continue;
+                    if (pj[c] >= 0) { spc[jl[c]] = sj[c]; path[jl[c]] = pj[c]; }
+                    tmin = fmin(tmin, sj[c]);
+                }
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, off));
