@@ -180,6 +180,10 @@ class DeviceCsrSolver:
         res.assignment = self.assign.ctypes.data_as(_lib._c_i64_p)
         res.hist_obj, res.hist_alpha = _lib.dptr(hobj), _lib.dptr(halpha)
         res.lot_sweeps = sweeps.ctypes.data_as(_lib._c_i32_p)
+        f64from = np.full(mi, -1, dtype=np.int32)
+        lot_ms = np.zeros(mi)
+        res.lot_fp64_from = f64from.ctypes.data_as(_lib._c_i32_p)
+        res.lot_ms = _lib.dptr(lot_ms)
         o = _opts(mi)
         _lib.check(self.lib.goat_fw_core_csr_device(self.h.ptr, n, ctypes.byref(self.structs[0]),
                                                     ctypes.byref(self.structs[1]), None, n, None, n,
@@ -188,6 +192,8 @@ class DeviceCsrSolver:
         self.phases = dict(zip(("gradient", "lot", "line_search", "lap", "setup", "total"),
                                [round(x, 2) for x in res.time_ms]))
         self.sweeps = sweeps[:it].tolist()
+        self.fp64_from = f64from[:it].tolist()
+        self.lot_ms = lot_ms[:it].tolist()
         self.alphas = halpha[1:it + 1].tolist()
         self.objective = float(res.objective)
         self.converged = bool(res.converged)
@@ -395,6 +401,7 @@ def run_ours(args):
     c5 = {"time_to_converge_ms": statistics.median(ms_steps), "iterations": iters // args.steps,
           "converged": solver.converged, "lot_sweeps": solver.sweeps, "alphas": solver.alphas,
           "phase_ms_last_step": solver.phases, "objective": solver.objective, "match_ratio": match,
+          "lot_fp64_from": solver.fp64_from, "lot_ms": [round(x, 2) for x in solver.lot_ms],
           "outer_iteration_ms": (solver.phases["gradient"] + solver.phases["lot"] + solver.phases["line_search"])
           / max(1, iters // args.steps), "host_generator_s": gen_s}
     del solver
@@ -425,6 +432,16 @@ def run_ours(args):
     torch.cuda.empty_cache()
     bytes_per_sweep = n * n * 4
     achieved = bytes_per_sweep / (msw * 1e-3) / 1e9
+    # the same kernel inside the timed solve: a LOT that ran its max_sweeps wholly in fp32
+    # is one launch of pre-check + sweeps + row-only pass, followed by the emit pass
+    # (one more read and one write of an n x n buffer) inside the same CUDA-event bracket
+    in_situ = None
+    for sw, f64, ms in zip(c5["lot_sweeps"], c5["lot_fp64_from"], c5["lot_ms"]):
+        if f64 < 0 and sw >= 100:
+            passes = sw + 2
+            in_situ = {"lot_ms": ms, "passes": passes, "ms_per_pass_incl_emit_and_minmax": ms / passes,
+                       "GB_s": (passes + 3) * bytes_per_sweep / (ms * 1e-3) / 1e9}
+            in_situ["frac"] = in_situ["GB_s"] / _peaks()[0]
     peak, peak_kind = _peaks()
     traffic, traffic_src = _traffic("sk_sweep_n40000_fp32")
     kernels = _kernel_scan(lib, h, dev, peak)
@@ -452,7 +469,7 @@ def run_ours(args):
                        "precision='fp32'))"},
         "roofline": {"kernel": "persistent log-domain Sinkhorn LOT sweep at n=40000 (one read of G per sweep)",
                      "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src, "in_situ": in_situ,
                      "note": f"{bytes_per_sweep} algorithmic bytes per sweep (n^2 fp32, one read of G), "
                              f"{msw * 1000:.1f} us per sweep averaged over a 52-sweep LOT launch "
                              f"(CUDA events on the library stream)"},

@@ -87,6 +87,7 @@ typedef struct goat_fw_result {
     double time_ms[6];       /* out: gradient, lot, linesearch+update, lap, h2d+setup, total */
     int32_t *lot_fp64_from;  /* [max_iters] out or NULL: fp32 handles, sweeps done in fp32 before the LOT
                               * finished in fp64 arithmetic (-1: the whole LOT ran in the handle's precision) */
+    double *lot_ms;          /* [max_iters] out or NULL: device time of each LOT step (CUDA events) */
 } goat_fw_result;
 
 int goat_create(goat_handle **out, const goat_config *cfg);

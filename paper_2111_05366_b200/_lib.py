@@ -46,7 +46,7 @@ class GoatFwResult(ctypes.Structure):
                 ("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
                 ("lap_certified", ctypes.c_int32), ("gpu_launches", ctypes.c_int32),
                 ("objective", ctypes.c_double), ("time_ms", ctypes.c_double * 6),
-                ("lot_fp64_from", _c_i32_p)]
+                ("lot_fp64_from", _c_i32_p), ("lot_ms", _c_double_p)]
 
 
 class GoatCsr(ctypes.Structure):

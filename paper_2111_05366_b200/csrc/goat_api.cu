@@ -524,6 +524,47 @@ LotOut run_lot(Ctx &c, const T *Gin, int sense, double lam, int max_sweeps, doub
     out.sweeps = h.h_state->sweeps;
     out.converged = h.h_state->converged;
     out.dev = h.h_state->dev;
+    if (getenv("GOAT_SK_VERBOSE")) {
+        fprintf(stderr, "lot n=%d sweeps %d converged %d dev %.3g fp64_from %d redone %d repaired %d\n", n, out.sweeps,
+                out.converged, out.dev, out.fp64_from, h.h_state->redone, h.h_state->repaired);
+        if (getenv("GOAT_SK_RETIME")) {
+            // diagnostics: the handle-precision sweep kernel timed alone on THIS cost matrix
+            // (50 sweeps that cannot converge), then the loop state is restored
+            const SkState keep = *h.h_state;
+            SkState st = st0;
+            st.tol = 1e-300; st.max_sweeps = 50;
+            *h.h_state = st;
+            GOAT_CUDA(cudaMemcpyAsync(a.st, h.h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
+            std::vector<double> fsave((size_t)c.ld * 4);
+            for (int q = 0; q < 2; ++q) {
+                GOAT_CUDA(cudaMemcpyAsync(fsave.data() + (size_t)q * c.ld, a.f[q], c.ld * 8, cudaMemcpyDeviceToHost, c.s));
+                GOAT_CUDA(cudaMemcpyAsync(fsave.data() + (size_t)(2 + q) * c.ld, a.g[q], c.ld * 8, cudaMemcpyDeviceToHost, c.s));
+            }
+            sync(c);
+            GOAT_CUDA(cudaMemsetAsync(a.f[0], 0, c.ld * 8, c.s));
+            GOAT_CUDA(cudaMemsetAsync(a.g[0], 0, c.ld * 8, c.s));
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0, c.s);
+            run_sweeps<T>(c, a, plan, 50);
+            cudaEventRecord(e1, c.s);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            fprintf(stderr, "lot n=%d retimed: %.3f ms per pass over 52 passes (redone %d repaired %d)\n", n, ms / 52.0,
+                    h.h_state->redone, h.h_state->repaired);
+            for (int q = 0; q < 2; ++q) {
+                GOAT_CUDA(cudaMemcpyAsync(a.f[q], fsave.data() + (size_t)q * c.ld, c.ld * 8, cudaMemcpyHostToDevice, c.s));
+                GOAT_CUDA(cudaMemcpyAsync(a.g[q], fsave.data() + (size_t)(2 + q) * c.ld, c.ld * 8, cudaMemcpyHostToDevice, c.s));
+            }
+            *h.h_state = keep;
+            GOAT_CUDA(cudaMemcpyAsync(a.st, h.h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
+            sync(c);
+        }
+    }
     double *part = h.red.as<double>();
     const int eb = kRedBlocks;
     sk_launch_emit<T>(a, Q, c.ld, P, c.ld, L, c.ld, part, eb, c.s);
@@ -711,7 +752,9 @@ void fw_loop(Ctx &c, bool have_L, bool p0_bary, const goat_options &o, goat_fw_r
                 launch_perm_matrix<T>(h.ivec.as<int>(), Q, ld, n, c.s);
                 lo.sweeps = 0; lo.converged = 1;
             }
-            t_lot += tm.stop();
+            const double t_this = tm.stop();
+            t_lot += t_this;
+            if (res->lot_ms) res->lot_ms[i - 1] = t_this;
         }
         if (res->lot_sweeps) res->lot_sweeps[i - 1] = lo.sweeps;
         if (res->lot_converged) res->lot_converged[i - 1] = lo.converged;

@@ -68,6 +68,7 @@ def _call_core(n, opts: MatchOptions, h, call):
     lconv = np.zeros(mi, dtype=np.int32)
     ldev = np.zeros(mi)
     f64from = np.full(mi, -1, dtype=np.int32)
+    lot_ms = np.zeros(mi)
     res = _lib.GoatFwResult()
     res.assignment = assign.ctypes.data_as(_lib._c_i64_p)
     res.hist_obj = _lib.dptr(hobj)
@@ -76,6 +77,7 @@ def _call_core(n, opts: MatchOptions, h, call):
     res.lot_converged = lconv.ctypes.data_as(_lib._c_i32_p)
     res.lot_dev = _lib.dptr(ldev)
     res.lot_fp64_from = f64from.ctypes.data_as(_lib._c_i32_p)
+    res.lot_ms = _lib.dptr(lot_ms)
     o = _lib.GoatOptions(
         max_iters=mi, max_sweeps=opts.sinkhorn.max_sweeps,
         sense=_lib.GOAT_MAXIMIZE if opts.objective_sense == "maximize" else _lib.GOAT_MINIMIZE,
@@ -88,7 +90,7 @@ def _call_core(n, opts: MatchOptions, h, call):
     history = [(0, float(hobj[0]), None)]
     history += [(i, float(hobj[i]), float(halpha[i])) for i in range(1, it + 1)]
     diag = dict(lot_sweeps=sweeps[:it].tolist(), lot_converged=lconv[:it].astype(bool).tolist(),
-                lot_deviation=ldev[:it].tolist(), lot_fp64_from=f64from[:it].tolist(),
+                lot_deviation=ldev[:it].tolist(), lot_fp64_from=f64from[:it].tolist(), lot_ms=lot_ms[:it].tolist(),
                 lap_certified=bool(res.lap_certified),
                 gpu_launches=int(res.gpu_launches), objective=float(res.objective),
                 time_ms=dict(zip(("gradient", "lot", "line_search", "lap", "setup", "total"),

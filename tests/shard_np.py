@@ -116,6 +116,11 @@ class NumpyShardBackend:
             self.badcol = ~(S > self.tiny) | ~np.isfinite(S)
             good = ~self.badcol
             dcol = float(np.max(np.abs(S[good] - 1.0), initial=0.0))
+            if k == 0 and self.badcol.any():
+                # an underflowed column of K is ~1 away from 1: the pre-check needs no
+                # exact sum (as sk_shard_merge_kernel)
+                dcol = max(dcol, 1.0)
+                self.badcol[:] = False
             if k != 0:
                 self.g[k & 1] = self.g[(k + 1) & 1].copy()
                 self.g[k & 1][good] = self.g[(k + 1) & 1][good] - np.log(S[good])
