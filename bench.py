@@ -274,7 +274,9 @@ def _dense_config(cfg, precision, dev_index, steps=2):
     d = r.diagnostics
     out = {"precision": precision, "n": A.shape[0], "solve_ms": 1000 * best, "iterations": r.iterations,
            "outer_iters_per_sec": r.iterations / best, "objective": r.objective,
-           "lot_sweeps": d["lot_sweeps"], "phase_ms": {k: round(v, 2) for k, v in d["time_ms"].items()},
+           "lot_sweeps": d["lot_sweeps"], "lot_fp64_from": d.get("lot_fp64_from"),
+           "lot_ms": [round(x, 2) for x in d.get("lot_ms", [])],
+           "phase_ms": {k: round(v, 2) for k, v in d["time_ms"].items()},
            "match_ratio": float(np.mean(r.alignment == truth))}
     gold = os.path.join(ROOT, "tests", "golden", "full_cases.npz")
     if cfg in (3, 4) and os.path.exists(gold):
@@ -453,6 +455,18 @@ def run_ours(args):
         secondary["c3_fp32"] = _dense_config(3, "fp32", local, steps=1)
     cpu = cpu_baseline(c5["lot_sweeps"] or [1000])
 
+    # the gradient's SpMM (two per gradient, one gradient per outer iteration): its real
+    # bound is the L2 gather of nnz rows of the dense operand, not the HBM algorithmic bytes
+    n_spmm = 2 * max(1, c5["iterations"])
+    ms_spmm = c5["phase_ms_last_step"]["gradient"] / n_spmm
+    nnz = float(A.indices.size + Bs.indices.size) / 2.0
+    spmm = {"kernel": "spmm_t_kernel (CSR x dense, transposed store)", "ms_per_spmm": ms_spmm,
+            "gathered_bytes": nnz * n * 4, "gathered_TB_s": nnz * n * 4 / (ms_spmm * 1e-3) / 1e12,
+            "algorithmic_bytes": 2.0 * n * n * 4 + nnz * 4 + (n + 1) * 8,
+            "algorithmic_GB_s": (2.0 * n * n * 4 + nnz * 4 + (n + 1) * 8) / (ms_spmm * 1e-3) / 1e9,
+            "note": "SURVEY 8(d): algorithmic bytes = read the dense operand once + write once + CSR; the kernel is "
+                    "bound by the L2 gather of nnz*n*4 bytes (ncu memory throughput 99 %, profiles/round1_ncu_pipe_spmm.md)"}
+
     line = {
         "metric": METRIC, "value": iters / (total_ms / 1000.0), "unit": "iter/s",
         "n_gpus": world, "steps": args.steps, "warmup": W,
@@ -470,10 +484,13 @@ def run_ours(args):
         "roofline": {"kernel": "persistent log-domain Sinkhorn LOT sweep at n=40000 (one read of G per sweep)",
                      "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src, "in_situ": in_situ,
-                     "note": f"{bytes_per_sweep} algorithmic bytes per sweep (n^2 fp32, one read of G), "
+                     "note": f"Sinkhorn is the largest share of the step (fp32 sk_wide_kernel + its fp64 finish, ~43 % of the "
+                             f"launch list; the single largest kernel after it is the gradient's SpMM, see gradient_spmm); "
+                             f"{bytes_per_sweep} algorithmic bytes per sweep (n^2 fp32, one read of G), "
                              f"{msw * 1000:.1f} us per sweep averaged over a 52-sweep LOT launch "
                              f"(CUDA events on the library stream)"},
         "cpu_baseline": cpu,
+        "gradient_spmm": spmm,
         "kernels": kernels,
         "secondary": secondary,
         "clocks": clocks.summary(),
