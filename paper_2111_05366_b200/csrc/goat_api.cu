@@ -407,7 +407,18 @@ struct LotOut {
 // Sweeps in fp32 arithmetic stop at this marginal deviation; below it an fp32
 // handle finishes the LOT in fp64 arithmetic (run_lot).  GOAT_SK_FP64_FINISH=0
 // keeps the pure-fp32 loop (measurement only: it cannot meet tol < floor).
-constexpr double kFp32DevFloor = 1e-4;
+constexpr double kFp32DevFloorDefault = 1e-4;
+// GOAT_SK_FP32_FLOOR overrides it (measurement: lower floors keep more sweeps in fp32
+// but approach the ~1e-6 noise of the fp32 deviation itself)
+inline double fp32_dev_floor() {
+    static const double v = [] {
+        const char *e = getenv("GOAT_SK_FP32_FLOOR");
+        const double x = e ? atof(e) : 0.0;
+        return x > 0.0 ? x : kFp32DevFloorDefault;
+    }();
+    return v;
+}
+#define kFp32DevFloor fp32_dev_floor()
 inline bool fp64_finish_enabled() {
     const char *e = getenv("GOAT_SK_FP64_FINISH");
     return !(e && atoi(e) == 0);
