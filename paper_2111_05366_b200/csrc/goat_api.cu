@@ -418,7 +418,6 @@ inline double fp32_dev_floor() {
     }();
     return v;
 }
-#define kFp32DevFloor fp32_dev_floor()
 inline bool fp64_finish_enabled() {
     const char *e = getenv("GOAT_SK_FP64_FINISH");
     return !(e && atoi(e) == 0);
@@ -492,14 +491,14 @@ LotOut run_lot(Ctx &c, const T *Gin, int sense, double lam, int max_sweeps, doub
     GOAT_CUDA(cudaMemsetAsync(a.g[0], 0, c.ld * 8, c.s));
     // fp32 arithmetic resolves the marginal deviation |u K v - 1| only down to
     // ~1e-5 (exponent rounding at |E + f + g| ~ 1e2), so a tolerance below
-    // kFp32DevFloor (the default 1e-8, sinkhorn.py:32) can never fire and every LOT
+    // fp32_dev_floor() (the default 1e-8, sinkhorn.py:32) can never fire and every LOT
     // would run max_sweeps.  fp32 handles therefore sweep in fp32 down to the
     // floor and finish in fp64 arithmetic on the same (exactly widened) fp32 G
     // from the same potentials, which restores the reference's stopping rule.
-    const bool finish64 = sizeof(T) == 4 && tol < kFp32DevFloor && fp64_finish_enabled();
+    const bool finish64 = sizeof(T) == 4 && tol < fp32_dev_floor() && fp64_finish_enabled();
     SkState st0{};
     st0.k = log_mode ? 1 : 0;
-    st0.gmax = gmax; st0.coef = coef; st0.tol = finish64 ? kFp32DevFloor : tol;
+    st0.gmax = gmax; st0.coef = coef; st0.tol = finish64 ? fp32_dev_floor() : tol;
     st0.max_sweeps = max_sweeps; st0.log_mode = log_mode;
     *h.h_state = st0;
     GOAT_CUDA(cudaMemcpyAsync(a.st, h.h_state, sizeof(SkState), cudaMemcpyHostToDevice, c.s));
@@ -1764,8 +1763,8 @@ int goat_shard_lot_begin(goat_handle *h, int32_t sense, double lam, double gmin,
             st0.coef = maximize ? -lam / scale : lam / scale;
             st0.log_mode = !(std::exp((-lam / scale) * scale) > 0.0);
             st0.k = st0.log_mode ? 1 : 0;
-            const bool finish64 = h->precision == GOAT_FP32 && tol < kFp32DevFloor && fp64_finish_enabled();
-            st0.tol = finish64 ? kFp32DevFloor : tol;
+            const bool finish64 = h->precision == GOAT_FP32 && tol < fp32_dev_floor() && fp64_finish_enabled();
+            st0.tol = finish64 ? fp32_dev_floor() : tol;
             st0.max_sweeps = max_sweeps;
         }
         S.user_tol = tol;
