@@ -2419,8 +2419,8 @@ __global__ void __launch_bounds__(kThreads) sk_shard_colsum_kernel(SkArgs a, int
     }
 }
 
-// One CTA: the gathered [world][n+1] rows merged in rank order (identical on every
-// rank), then the stopping rule of sk_sweeps and g_k = g_{k-1} - log(colsum).
+// The gathered [world][n+1] rows merged in rank order (identical on every rank), then
+// the stopping rule of sk_sweeps and g_k = g_{k-1} - log(colsum).
 // A column sum that under/overflows (fp32: every entry below the ex2 range) is
 // flagged in bad[] and the sweep is left pending: sk_shard_repair_pass/merge then
 // compute those columns' exact fp64 LSE across all ranks, as sk_exact_col does
@@ -2443,14 +2443,19 @@ __device__ __forceinline__ double block_max_1024(double v, double *s_red) {
     return r;
 }
 
+// Several CTAs split the columns (a single CTA took 84 us per sweep at n = 40000 -- half of a
+// rank's pass time at 8 GPUs); each leaves its (max column deviation, flagged-column count) in
+// devcol[2 * blk ..] and the LAST CTA to finish -- st->arrive counts them -- applies the
+// stopping rule and advances the loop state, so no CTA reads the state after it was advanced.
+// Every quantity is a max or an integer sum: the result does not depend on which CTA is last.
 __global__ void __launch_bounds__(kShardMergeThreads) sk_shard_merge_kernel(SkArgs a, const double *recv, int world,
                                                                             double tiny, unsigned char *bad) {
     __shared__ double s_red[kShardMergeThreads / 32];
-    __shared__ int s_bad;
+    __shared__ int s_bad, s_last;
     SkState *st = a.st;
-    if (*(volatile int *)&st->done || *(volatile int *)&st->pending) return;
+    if (*(volatile int *)&st->done || *(volatile int *)&st->pending) return;  // no CTA of this launch writes them before all have read
     const int tid = threadIdx.x;
-    const int k = st->k, K = st->max_sweeps, n = a.n;
+    const int k = *(volatile int *)&st->k, K = st->max_sweeps, n = a.n;
     const int64_t ld1 = (int64_t)n + 1;
     const double tol = st->tol;
     const bool pre = (k == 0);
@@ -2463,42 +2468,58 @@ __global__ void __launch_bounds__(kShardMergeThreads) sk_shard_merge_kernel(SkAr
         else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
     }
     __syncthreads();
-    if (stop) {
-        if (tid == 0) { st->dev = drow; shard_finish(st, k, stop, sweeps, conv, slot); }
-        return;
-    }
     double dcol = 0.0;
     int nbad = 0;
-    const double *gold = gslot(a, k + 1);
-    double *gnew = gslot(a, k);
-    for (int j = tid; j < n; j += kShardMergeThreads) {
-        double S = 0.0;
-        for (int r = 0; r < world; ++r) S += recv[r * ld1 + j];
-        bool b = !(S > tiny) || !isfinite(S);
-        if (pre && b) {  // an underflowed column of K is ~1 away from 1: no exact sum needed (merge_body)
-            dcol = fmax(dcol, 1.0);
-            b = false;
-            bad[j] = 0;
-            continue;
+    if (!stop) {
+        const double *gold = gslot(a, k + 1);
+        double *gnew = gslot(a, k);
+        for (int j = blockIdx.x * kShardMergeThreads + tid; j < n; j += gridDim.x * kShardMergeThreads) {
+            double S = 0.0;
+            for (int r = 0; r < world; ++r) S += recv[r * ld1 + j];
+            bool b = !(S > tiny) || !isfinite(S);
+            if (pre && b) {  // an underflowed column of K is ~1 away from 1: no exact sum needed (merge_body)
+                dcol = fmax(dcol, 1.0);
+                bad[j] = 0;
+                continue;
+            }
+            bad[j] = b;
+            nbad += b;
+            if (b) continue;
+            if (pre) dcol = fmax(dcol, fabs(S - 1.0));
+            else gnew[j] = gold[j] - log(S);
         }
-        bad[j] = b;
-        nbad += b;
-        if (b) continue;
-        if (pre) dcol = fmax(dcol, fabs(S - 1.0));
-        else gnew[j] = gold[j] - log(S);
     }
     if (nbad) atomicAdd(&s_bad, nbad);
     dcol = block_max_1024(dcol, s_red);  // includes the barrier that publishes s_bad
-    if (tid != 0) return;
-    if (s_bad) {  // the repair round finishes this sweep
-        st->repaired += s_bad;
-        st->dcol = dcol;
+    if (tid == 0) {
+        __stcg(a.devcol + 2 * blockIdx.x, dcol);
+        __stcg(a.devcol + 2 * blockIdx.x + 1, (double)s_bad);
+        __threadfence();
+        s_last = (atomicAdd(&st->arrive, 1) == (int)gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last || tid != 0) return;
+    __threadfence();
+    st->arrive = 0;
+    if (stop) {
+        st->dev = drow;
+        shard_finish(st, k, stop, sweeps, conv, slot);
+        return;
+    }
+    double dc = 0.0, nb = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+        dc = fmax(dc, __ldcg(a.devcol + 2 * b));
+        nb += __ldcg(a.devcol + 2 * b + 1);
+    }
+    if (nb > 0.0) {  // the repair round finishes this sweep
+        st->repaired += (int)nb;
+        st->dcol = dc;
         st->last_dev = drow;
         st->pending = 1;
         return;
     }
     if (pre) {
-        const double d0 = fmax(drow, dcol);
+        const double d0 = fmax(drow, dc);
         if (d0 < tol) { stop = 1; sweeps = 0; conv = 1; slot = 0; st->dev = d0; }
         st->last_dev = d0;
     }
@@ -3479,7 +3500,8 @@ void sk_launch_shard_pass(const SkArgs &a, const SkPlan &p, unsigned *bar, doubl
 template <class T>
 void sk_launch_shard_merge(const SkArgs &a, const double *recv, int world, unsigned char *bad, cudaStream_t s) {
     const double tiny = sizeof(T) == 4 ? 1e-30 : 1e-290;
-    sk_shard_merge_kernel<<<1, kShardMergeThreads, 0, s>>>(a, recv, world, tiny, bad);
+    const int blocks = std::max(1, std::min(64, ceil_div(a.n, kShardMergeThreads)));
+    sk_shard_merge_kernel<<<blocks, kShardMergeThreads, 0, s>>>(a, recv, world, tiny, bad);
     note_launch();
     GOAT_CHECK_LAUNCH();
 }

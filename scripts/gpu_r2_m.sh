@@ -1,4 +1,6 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-GOAT_LAP_VERBOSE=1 timeout 900 python -m pytest tests/test_lap_auction_gpu.py -q -x -p no:cacheprovider -k "12000" -s > gpurun_out/r2m_tests.log 2>&1
-grep "lap \|passed\|failed\|Error" gpurun_out/r2m_tests.log | cut -c1-250
+timeout 900 python -m pytest tests/test_sharded_gpu.py -q -p no:cacheprovider 2>&1 | tail -2
+GOAT_SK_FP64_FINISH=0 python scripts/prof_shard_sweep.py 40000 100 fp32 2>&1 | tail -1
+python scripts/prof_shard_sweep.py 40000 30 fp64 2>&1 | tail -1
+GOAT_SK_FP64_FINISH=0 python scripts/prof_shard_sweep.py 5000 200 fp32 2>&1 | tail -1
