@@ -82,6 +82,7 @@ struct SkState {
     double dcol;    // row-sharded pre-check: column deviation of the columns that needed no repair
     int redone;     // wide fp32 rows: sweeps recomputed with the max shift (diagnostic)
     int nostop_k;   // a resumed LOT: the convergence test may not fire at passes <= nostop_k (0 = none)
+    int redo_next;  // row-sharded driver: the next pass repeats sweep k with the max shift (a row left the fixed-shift window on some rank)
 };
 
 // Count of kernels this library launched (reported as gpu_launches).

@@ -1609,7 +1609,9 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) sk_pipe_kernel(SkArgs a
     };
     // redo flags (one per sweep parity) share the barrier scratch: bytes [256, 264)
     unsigned *redo = bar + 64;
-    const bool shift_ok = rg.nrows <= kPipeShiftRows && !a.single_pass && env_shift_ok(a);
+    // single-pass launches (row-sharded driver) take the fixed shift too; a row that leaves
+    // the window on any rank makes every rank repeat the sweep with the max shift (redo_next)
+    const bool shift_ok = rg.nrows <= kPipeShiftRows && env_shift_ok(a) && !(a.single_pass && a.st->redo_next);
     for (int k = k0;; ++k) {
         bool maxp = !shift_ok || k <= 1;
         for (;;) {
@@ -2309,7 +2311,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) sk_wide_kernel(SkArgs
         }
     };
     unsigned *redo = bar + 64;
-    const bool shift_ok = !a.single_pass && env_shift_ok(a);
+    const bool shift_ok = env_shift_ok(a) && !(a.single_pass && a.st->redo_next);
     for (int k = k0;; ++k) {
         bool maxp = !shift_ok || k <= 1;
         for (;;) {
@@ -2402,7 +2404,8 @@ void *wide2_for(int nt, int cl, int ch, bool tm = false, int cc = 2) {
 // ------------------------------------------------------------------ row-sharded sweep
 // Column sums of this block's pass (fixed CTA order, fp64) and its max row deviation.
 template <class T>
-__global__ void __launch_bounds__(kThreads) sk_shard_colsum_kernel(SkArgs a, int pass_blocks, double *send) {
+__global__ void __launch_bounds__(kThreads) sk_shard_colsum_kernel(SkArgs a, int pass_blocks, double *send,
+                                                                   const unsigned *redo) {
     if (*(volatile int *)&a.st->done || *(volatile int *)&a.st->pending) return;
     const int n = a.n, np = a.nblk;
     const T *cp = static_cast<const T *>(a.colpart);
@@ -2415,7 +2418,9 @@ __global__ void __launch_bounds__(kThreads) sk_shard_colsum_kernel(SkArgs a, int
         double d = 0.0;
         for (int b = threadIdx.x; b < pass_blocks; b += 32) d = fmax(d, __ldcg(a.devpart + b));
         for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
-        if (threadIdx.x == 0) send[n] = d;
+        // a fixed-shift pass that left the window on this rank: its column sums are void, and
+        // an infinite deviation tells every rank's merge to repeat the sweep with the max shift
+        if (threadIdx.x == 0) send[n] = __ldcg(redo + (*(volatile int *)&a.st->k & 1)) ? INFINITY : d;
     }
 }
 
@@ -2462,15 +2467,17 @@ __global__ void __launch_bounds__(kShardMergeThreads) sk_shard_merge_kernel(SkAr
     if (tid == 0) s_bad = 0;
     double drow = 0.0;
     for (int r = 0; r < world; ++r) drow = fmax(drow, recv[r * ld1 + n]);
+    // some rank's fixed-shift pass left the window (colsum kernel): repeat sweep k with the max shift
+    const bool redo = isinf(drow) && !st->redo_next;
     int stop = 0, sweeps = 0, conv = 0, slot = 0;
-    if (k >= 2) {
+    if (k >= 2 && !redo) {
         if (drow < tol && k > st->nostop_k) { stop = 1; sweeps = k - 1; conv = 1; slot = (k - 1) & 1; }
         else if (k == K + 1) { stop = 1; sweeps = K; conv = 0; slot = K & 1; }
     }
     __syncthreads();
     double dcol = 0.0;
     int nbad = 0;
-    if (!stop) {
+    if (!stop && !redo) {
         const double *gold = gslot(a, k + 1);
         double *gnew = gslot(a, k);
         for (int j = blockIdx.x * kShardMergeThreads + tid; j < n; j += gridDim.x * kShardMergeThreads) {
@@ -2501,6 +2508,12 @@ __global__ void __launch_bounds__(kShardMergeThreads) sk_shard_merge_kernel(SkAr
     if (!s_last || tid != 0) return;
     __threadfence();
     st->arrive = 0;
+    if (redo) {
+        st->redo_next = 1;
+        st->redone += 1;
+        return;  // k unchanged: the next pass repeats it
+    }
+    st->redo_next = 0;
     if (stop) {
         st->dev = drow;
         shard_finish(st, k, stop, sweeps, conv, slot);
@@ -3492,7 +3505,7 @@ void sk_launch_shard_pass(const SkArgs &a, const SkPlan &p, unsigned *bar, doubl
     sk_launch_persistent<T>(args, p, bar, s);
     args.nblk = p.ngrp;
     sk_shard_colsum_kernel<T><<<std::max(1, std::min(ceil_div(a.n, kThreads), 4 * 148)), kThreads, 0, s>>>(
-        args, p.nblk, send);
+        args, p.nblk, send, bar + 64);
     note_launch();
     GOAT_CHECK_LAUNCH();
 }
